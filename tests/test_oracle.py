@@ -1,0 +1,116 @@
+"""Pin the CPU oracle (oracle/ws_oracle.c) to the reference's own outputs.
+
+Every fixture under tests/golden/ was produced by running the reference
+package itself (tests/golden/make_golden.py).  The oracle must reproduce,
+op for op: statuses / found flags / values, per-op probe counts (distinct
+128-B lines, reference instrument.py:26-85), lock touches, the final raw
+slot-key layout (slot positions, reference tables/openaddr.py:132-185),
+fingerprint tags, and for chaining the node numbering.  Only once this file
+passes is the oracle trusted as the checker for the CUDA path.
+"""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import OracleTable, build_oracle
+from paper_2509_16407_b200.core import TableConfig
+
+FIXTURES = sorted(glob.glob(os.path.join(GOLDEN, "ops_*.npz")))
+
+
+def _load(path):
+    z = np.load(path)
+    name = os.path.basename(path)[4:-4]
+    design = name.rsplit("_", 1)[0]
+    extra = json.loads(str(z["extra"][0]))
+    cfg = TableConfig(design=design, capacity_slots=int(z["capacity"][0]),
+                      seed=int(z["seed"][0]), **extra)
+    return z, cfg
+
+
+def setup_module(_m):
+    build_oracle()
+
+
+@pytest.mark.parametrize("path", FIXTURES, ids=lambda p: os.path.basename(p)[4:-4])
+def test_oracle_replays_reference_stream(path):
+    z, cfg = _load(path)
+    t = OracleTable(cfg)
+    probes = np.zeros(len(z["ops"]), dtype=np.uint32)
+    status, qvals = t.mixed_batch(z["ops"], z["keys"], z["vals"], probes=probes)
+    np.testing.assert_array_equal(status, z["status"])
+    np.testing.assert_array_equal(qvals, z["qvals"])
+    np.testing.assert_array_equal(probes, z["probes"])
+    assert t.lock_touches == int(z["lock_touches"][0])
+    k, v = t.items_arrays()
+    np.testing.assert_array_equal(k, z["item_keys"])
+    np.testing.assert_array_equal(v, z["item_vals"])
+    if cfg.design == "chaining":
+        assert t.next_node == int(z["next_node"][0])
+        assert t.arena_capacity == int(z["arena_capacity"][0])
+        w = t.words()
+        ref = z["words"]
+        keys_ref = ref.reshape(-1, 16)[:, :14:2]
+        keys_got = w.reshape(-1, 16)[:, :14:2]
+        np.testing.assert_array_equal(keys_got, keys_ref)
+        np.testing.assert_array_equal(w.reshape(-1, 16)[:, 14], ref.reshape(-1, 16)[:, 14])
+    else:
+        np.testing.assert_array_equal(t.slot_keys(), z["slot_keys"])
+        if "tags" in z.files:
+            np.testing.assert_array_equal(t.tags(), z["tags"])
+    assert t.duplicate_scan() == {}
+
+
+def test_hash_kat_against_reference_fixture():
+    from paper_2509_16407_b200 import core
+    kat = json.load(open(os.path.join(GOLDEN, "hash_kat.json")))
+    for seed, seeds in kat["families"].items():
+        assert [str(s) for s in core.HashFamily(int(seed), 8).seeds] == seeds
+    for x, y in kat["mix64"]:
+        assert core.mix64(int(x)) == int(y)
+    fam = core.HashFamily(42, 4)
+    for key, nb, b0, b1, b2, tag in kat["buckets"]:
+        key = int(key)
+        assert (fam.bucket(0, key, nb), fam.bucket(1, key, nb), fam.bucket(2, key, nb)) == (b0, b1, b2)
+        assert core.fingerprint(fam, key) == tag
+    for cap, front, back in kat["iceberg"]:
+        d = core.derive(TableConfig(design="iceberg", capacity_slots=cap))
+        assert (d.front_buckets, d.back_buckets) == (front, back)
+
+
+def test_config_validation_matches_reference():
+    from paper_2509_16407_b200 import core
+    kat = json.load(open(os.path.join(GOLDEN, "hash_kat.json")))
+    for fields, outcome, detail in kat["configs"]:
+        try:
+            cfg = core.validate_config(TableConfig(**fields))
+            got = ("ok", cfg.bucket_size)
+        except core.ConfigError as e:
+            got = ("error", e.problems)
+        assert got == (outcome, detail), fields
+
+
+def test_key_generators_match_reference():
+    from paper_2509_16407_b200 import workload
+    kat = json.load(open(os.path.join(GOLDEN, "hash_kat.json")))
+    for seed, keys in kat["keys"].items():
+        got = workload.gen_uniform_keys(int(seed), len(keys)).tolist()
+        assert [str(k) for k in got] == keys
+    for parts, want in kat["derive_seed"]:
+        assert workload.derive_seed(*[int(p) for p in parts]) == int(want)
+
+
+def test_oracle_sequential_matches_survey_kats():
+    # seed 42, nb = 2^23
+    from paper_2509_16407_b200 import core
+    fam = core.HashFamily(42, 4)
+    assert fam.seeds[0] == 0xBDD732262FEB6E95
+    assert fam.raw(0, 1) == 0xC69F3558819AF2C8
+    assert fam.bucket(0, 1, 1 << 23) == 5800346
+    assert fam.bucket(1, 1, 1 << 23) == 1511528
+    assert core.fingerprint(fam, 0x123456789ABCDEF0) == 0xBC36
