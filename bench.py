@@ -1,0 +1,358 @@
+"""Benchmark: P2-MD (power-of-two-choice + fingerprint metadata) hash table,
+insert to 0.9 load then 50/50 hit/miss lock-free queries (BASELINE.json
+config 2: 2^28 slots on one B200).
+
+One step = clear the table, insert n = int(0.9 * slots) uniform keys
+(values k & 0xFFFF, reference runners.py:104) in one batch, then query n keys
+(half inserted, half absent, shuffled) in one batch.  Inputs are generated
+once and stay resident in HBM; the table (4.5 GiB) and the key batches
+(1.9 GiB each) dwarf the 126 MB L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  --impl reference times the reference's
+algorithm on the host CPU (oracle/ C port of warpbench's P2MdTable, one table
+shard per host thread) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mops/s insert+query at 0.9 load, 1/2/4/8 B200; % HBM random-access roofline"
+UNIT = "Mops/s"
+# algorithmic HBM bytes per op: random table traffic
+# from SURVEY 8(d) plus the streaming batch I/O (key 8 + value 8 + status 1)
+INSERT_TABLE_B = 175.0
+QUERY_TABLE_B = 116.0
+INSERT_IO_B = 17.0
+QUERY_IO_B = 17.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log2-slots", type=int, default=28)
+    ap.add_argument("--load", type=float, default=0.9)
+    ap.add_argument("--design", default="p2_md")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self._nv:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def report(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+
+
+# ------------------------------------------------------------- CPU leg
+
+def cpu_port_rate(n_slots: int, load: float, threads: int, seed: int = 42):
+    """Reference algorithm (oracle C port of P2MdTable) on `threads` host
+    threads, each owning an independent 1/threads shard of the table; returns
+    (Mops/s for insert+query, seconds, description)."""
+    from oracle import OracleTable, build_oracle
+    from paper_2509_16407_b200.core import TableConfig
+    from paper_2509_16407_b200.workload import derive_seed, gen_uniform_keys
+    build_oracle()
+    per = n_slots // threads
+    per -= per % 32
+    n = int(per * load)
+    shards = []
+    for i in range(threads):
+        keys = gen_uniform_keys(derive_seed(seed, i), n)
+        miss = gen_uniform_keys(derive_seed(seed, 0xFEED, i), n - n // 2)
+        q = np.concatenate([keys[: n // 2], miss])
+        np.random.default_rng(i).shuffle(q)
+        shards.append((OracleTable(TableConfig(design="p2_md", capacity_slots=per, seed=seed)),
+                       keys, keys & np.uint64(0xFFFF), q))
+
+    def work(s):
+        t, k, v, q = s
+        t.upsert_batch(k, v)
+        t.query_batch(q)
+
+    ths = [threading.Thread(target=work, args=(s,)) for s in shards]
+    t0 = time.perf_counter()
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    dt = time.perf_counter() - t0
+    ops = 2 * n * threads
+    return ops / dt / 1e6, dt, (f"p2_md {threads} shard(s) x {per} slots, {n} inserts + {n} "
+                                 f"50/50 queries per shard ({ops} ops)")
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample_slots = 1 << 23
+    rates = []
+    for _ in range(args.warmup):
+        cpu_port_rate(sample_slots, args.load, threads)
+    t_all = 0.0
+    desc = ""
+    for _ in range(args.steps):
+        r, dt, desc = cpu_port_rate(sample_slots, args.load, threads)
+        rates.append(r)
+        t_all += dt
+    v = statistics.median(rates)
+    out = {
+        "metric": METRIC, "value": round(v, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * t_all / max(1, args.steps), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (numpy PCG64 uniform keys, reference bench/keys.py)",
+        "impl": "reference",
+        "config": {"workload": f"{args.design} insert to {args.load} load then 50/50 queries "
+                               f"(bounded CPU sample of 2^{sample_slots.bit_length() - 1} slots)",
+                   "design": args.design, "log2_slots": sample_slots.bit_length() - 1,
+                   "load": args.load},
+        "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------- GPU leg
+
+def run_ours(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_16407_b200 import TableConfig, make_table
+    from paper_2509_16407_b200.workload import derive_seed, gen_uniform_keys
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    slots = 1 << args.log2_slots
+    cfg = TableConfig(design=args.design, capacity_slots=slots, seed=42)
+    table = make_table(cfg)
+    n = int(slots * args.load)
+    seed = derive_seed(42, rank)
+    keys_h = gen_uniform_keys(seed, n)
+    vals_h = keys_h & np.uint64(0xFFFF)
+    miss_h = gen_uniform_keys(derive_seed(seed, 0xFEED), n - n // 2)
+
+    def dev_u64(a):
+        return torch.from_numpy(a.view(np.int64)).to(dev).view(torch.uint64)
+
+    keys = dev_u64(keys_h)
+    vals = dev_u64(vals_h)
+    q = torch.cat([keys[: n // 2], dev_u64(miss_h)])
+    q = q[torch.randperm(n, device=dev, generator=torch.Generator(device=dev).manual_seed(1))]
+    stream = torch.cuda.current_stream(dev)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def step(i=None):
+        table.clear()
+        if i is not None:
+            ev[i][0].record(stream)
+        st = table.upsert_batch(keys, vals, check=False)
+        if i is not None:
+            ev[i][1].record(stream)
+        found, qv = table.query_batch(q, check=False)
+        if i is not None:
+            ev[i][2].record(stream)
+        return st, found, qv
+
+    # correctness gate on the first warm-up step (not timed)
+    st, found, qv = step()
+    torch.cuda.synchronize()
+    bad = int((st != 0).sum())
+    hits = int(found.sum())
+    assert bad == 0, f"{bad} inserts did not report INSERTED"
+    assert hits == n // 2, f"expected {n // 2} query hits, got {hits}"
+    for _ in range(max(0, args.warmup - 1)):
+        step()
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    ms_ins = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    ms_qry = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ops_per_step = 2 * n * world
+    value = ops_per_step * args.steps / (ms / 1000) / 1e6
+
+    # e2e through the C ABI with pinned HOST buffers (H2D + D2H inside)
+    kh = torch.from_numpy(keys_h.view(np.int64)).pin_memory()
+    vh = torch.from_numpy(vals_h.view(np.int64)).pin_memory()
+    qh = q.cpu().pin_memory()
+    e2e_times = []
+    for _ in range(max(1, args.e2e_steps)):
+        table.clear()
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        st_h = table.upsert_batch(kh.view(torch.uint64), vh.view(torch.uint64))
+        f_h, v_h = table.query_batch(qh.view(torch.uint64))
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - a)
+    assert int(st_h.sum()) == 0 and int(f_h.sum()) == n // 2
+    e2e_s = statistics.median(e2e_times)
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_val = ops_per_step / e2e_s / 1e6
+
+    if rank != 0:
+        return
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    ins_bytes = (INSERT_TABLE_B + INSERT_IO_B) * n
+    qry_bytes = (QUERY_TABLE_B + QUERY_IO_B) * n
+    ins_gbs = ins_bytes / (ms_ins / 1000) / 1e9
+    qry_gbs = qry_bytes / (ms_qry / 1000) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("insert_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = 1
+        r, dt, desc = cpu_port_rate(1 << 22, args.load, threads)
+        cpu = {"value": round(r, 3), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": desc + f"; {dt:.2f} s"}
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (numpy PCG64 uniform keys, reference bench/keys.py; values k & 0xFFFF)",
+        "config": {
+            "workload": f"{args.design} 2^{args.log2_slots} slots/GPU: insert {n} keys to "
+                        f"{args.load} load, then {n} 50/50 hit/miss lock-free queries",
+            "design": args.design, "log2_slots_per_gpu": args.log2_slots, "load": args.load,
+            "ops_per_step": ops_per_step, "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+            "l2": "table 4.5 GiB and key batches 1.9 GiB exceed the 126 MB L2; no flush",
+            "insert_ms": round(ms_ins, 3), "query_ms": round(ms_qry, 3),
+            "insert_mops": round(n / ms_ins / 1e3, 1), "query_mops": round(n / ms_qry / 1e3, 1),
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": "k_ops<P2_MD> (upsert)", "achieved": round(ins_gbs, 1),
+            "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ins_gbs / peak, 4),
+            "traffic": traffic,
+            "algorithmic_bytes_per_op": INSERT_TABLE_B + INSERT_IO_B,
+            "query_kernel": {"kernel": "k_query<P2_MD>", "achieved": round(qry_gbs, 1),
+                             "frac": round(qry_gbs / peak, 4),
+                             "algorithmic_bytes_per_op": QUERY_TABLE_B + QUERY_IO_B},
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
+                "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(n * 10),
+                "path": "ws_upsert/ws_query C ABI with pinned host buffers"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.report(),
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/* warpspeed.h -- C ABI of the B200-native WarpSpeed hash-table hot path.
+ *
+ * libwarpspeed.so (built from paper_2509_16407_b200/csrc/) exports exactly the
+ * functions below.  Signatures use plain pointers and sizes only; pointers may
+ * be device memory (e.g. torch CUDA tensors' data_ptr) or host memory (pinned
+ * or pageable).  Host buffers are staged through the table's device buffers
+ * with the copies pipelined against the kernels, so an FFI caller with plain
+ * host arrays (ctypes / cgo / JNI) can use the table directly.
+ *
+ * The reference (warpbench, pure Python) has no FFI; each entry point replaces
+ * the Python surface named beside it (paths under /root/reference/pkg/src/warpbench):
+ *
+ *   ws_create / ws_destroy    make_table(TableConfig)          tables/__init__.py:30-35
+ *                             HashTable.__init__               tables/base.py:57-73
+ *   ws_clear                  (new) make_table() again without reallocating
+ *   ws_upsert                 HashTable.upsert(key, value, merge)  tables/base.py:115-124
+ *   ws_query                  HashTable.query(key)             tables/base.py:126-129
+ *   ws_erase                  HashTable.erase(key)             tables/base.py:131-134
+ *   ws_mixed                  concurrent mixed phase (aging mixed_worker)  bench/runners.py:282-295
+ *   ws_locate                 HashTable.slot_of(key)           tables/base.py:136-143
+ *   ws_probe_counts           upsert/query/erase(..., probe=ProbeRecorder)  instrument.py:26-85
+ *   ws_export_items           HashTable.items()                tables/base.py:147-149
+ *   ws_occupied               HashTable.occupied_count()       tables/base.py:158-162
+ *   ws_duplicate_scan         HashTable.duplicate_scan()       tables/base.py:151-156
+ *   ws_checksum               (new) size-independent content digest for parity at 2^28+
+ *   ws_export_raw             slots.key_at / tags.get / arena words (test introspection)
+ *   ws_info                   storage_report / arena.next_node / _tombstones_ever
+ *   ws_strerror               exception messages (InvalidKeyError / ConfigError)
+ *
+ * Semantics: a batch is a set of operations that execute concurrently on the
+ * device; every op is linearizable.  Ops on the same key inside one batch are
+ * serialised by the key's primary-bucket lock in an unspecified order, so a
+ * batch's outcome is deterministic whenever its merges commute (ADD / MAX /
+ * MIN) and erase / upsert / query roles are key-disjoint.  A batch holding any
+ * sentinel key (0, 2^64-1, 2^64-2) is rejected as a whole before any mutation
+ * (reference core.py:103-117).
+ */
+#ifndef WARPSPEED_H
+#define WARPSPEED_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define WS_API __attribute__((visibility("default")))
+#else
+#define WS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes */
+#define WS_OK 0
+#define WS_ERR_INVALID_KEY (-1) /* sentinel key in batch; table untouched */
+#define WS_ERR_CONFIG (-2)
+#define WS_ERR_CUDA (-3)
+#define WS_ERR_ALLOC (-4)
+#define WS_ERR_ARG (-5)
+#define WS_ERR_INVALID_OP (-6)
+
+/* designs (same order as reference core.py:40-50 DESIGNS) */
+enum {
+  WS_DESIGN_DOUBLE = 0, WS_DESIGN_DOUBLE_MD, WS_DESIGN_P2, WS_DESIGN_P2_MD,
+  WS_DESIGN_ICEBERG, WS_DESIGN_ICEBERG_MD, WS_DESIGN_CUCKOO, WS_DESIGN_CHAINING,
+  WS_DESIGN_UNSAFE_REFERENCE
+};
+/* merge callbacks as a device enum (reference merge(existing, new) callables) */
+enum { WS_MERGE_REPLACE = 0, WS_MERGE_KEEP, WS_MERGE_ADD, WS_MERGE_MAX, WS_MERGE_MIN };
+/* upsert status (reference UpsertStatus, tables/base.py:42-45) */
+enum { WS_INSERTED = 0, WS_UPDATED = 1, WS_FULL = 2 };
+/* mixed-op byte: kind | merge << 4 */
+enum { WS_OP_UPSERT = 0, WS_OP_ERASE = 1, WS_OP_QUERY = 2 };
+
+/* call flags */
+#define WS_F_SYNC_CHECK 1u  /* validate keys synchronously, return WS_ERR_INVALID_KEY */
+#define WS_F_NO_CHECK 2u    /* caller guarantees no sentinels */
+#define WS_F_SERIAL 4u      /* one device thread runs the batch in index order:
+                               exactly the reference's sequential semantics */
+
+/* All derived integers are computed by the host layer exactly as the
+ * reference computes them (core.py:209-211, openaddr.py:45-47,351-352,505-507). */
+typedef struct ws_config {
+  int32_t design;
+  int32_t bucket_size;
+  uint64_t capacity_slots;
+  uint64_t front_buckets;   /* iceberg: round(nb * fraction), clamped */
+  uint64_t seeds[8];        /* HashFamily(seed).seeds */
+  int32_t n_seeds;
+  int32_t shortcut_slots;   /* int(shortcut_threshold * bucket_size) */
+  int32_t zero_count_cap;   /* max(1, bucket_size - shortcut_slots + 1) */
+  int32_t probe_cap;
+  int32_t ways;             /* cuckoo_ways */
+  int32_t path_depth;       /* cuckoo_path_depth */
+  int32_t phased;           /* mode == "phased": no locks, weak loads */
+  int32_t line_bytes;
+  int32_t multi_stream;     /* launches may run concurrently on several streams */
+  uint64_t chain_pool_nodes;/* chaining: initial physical node pool (0 = default) */
+} ws_config;
+
+typedef struct ws_info_t {
+  uint64_t capacity_slots, num_buckets, primary_buckets;
+  uint64_t slot_bytes, tag_bytes, lock_bytes, node_bytes; /* device allocation */
+  uint64_t next_node, pool_nodes;                         /* chaining */
+  int32_t tombstones_ever;
+  int32_t device;
+} ws_info_t;
+
+typedef struct ws_table ws_table;
+
+WS_API int ws_create(const ws_config *cfg, int device, ws_table **out);
+WS_API int ws_destroy(ws_table *t);
+/* reset to the freshly-created state (all slots EMPTY, flags cleared) */
+WS_API int ws_clear(ws_table *t, void *stream);
+
+WS_API int ws_upsert(ws_table *t, const uint64_t *keys, const uint64_t *vals, uint64_t n,
+              uint32_t merge, uint8_t *status, void *stream, uint32_t flags);
+WS_API int ws_query(ws_table *t, const uint64_t *keys, uint64_t n, uint64_t *vals_out,
+             uint8_t *found, void *stream, uint32_t flags);
+WS_API int ws_erase(ws_table *t, const uint64_t *keys, uint64_t n, uint8_t *found,
+             void *stream, uint32_t flags);
+WS_API int ws_mixed(ws_table *t, const uint8_t *ops, const uint64_t *keys, const uint64_t *vals,
+             uint64_t n, uint8_t *status, uint64_t *vals_out, void *stream, uint32_t flags);
+
+/* slot index of each key (-1 if absent); chaining: node*bucket_size + pair */
+WS_API int ws_locate(ws_table *t, const uint64_t *keys, uint64_t n, int64_t *slot_out, void *stream);
+
+/* instrumented mixed batch: probes[i] = distinct line regions op i touched,
+ * *lock_touches = total lock-word touches (reference ProbeRecorder semantics) */
+WS_API int ws_probe_counts(ws_table *t, const uint8_t *ops, const uint64_t *keys,
+                    const uint64_t *vals, uint64_t n, uint8_t *status, uint64_t *vals_out,
+                    uint32_t *probes, uint64_t *lock_touches, void *stream, uint32_t flags);
+
+/* quiescent introspection (synchronous) */
+WS_API int ws_occupied(ws_table *t, uint64_t *count_out, void *stream);
+WS_API int ws_export_items(ws_table *t, uint64_t *keys, uint64_t *vals, uint64_t cap,
+                    uint64_t *n_out, void *stream);
+WS_API int ws_duplicate_scan(ws_table *t, uint64_t *dup_keys, uint64_t *dup_counts, uint64_t cap,
+                      uint64_t *n_dup_out, void *stream);
+/* out[0]=occupied, [1]=sum keys, [2]=sum values, [3]=xor of mix64(k ^ mix64(v)) */
+WS_API int ws_checksum(ws_table *t, uint64_t out[4], void *stream);
+WS_API int ws_export_raw(ws_table *t, uint64_t *words, uint64_t nwords, uint16_t *tags,
+                  void *stream);
+WS_API int ws_info(ws_table *t, ws_info_t *info);
+
+WS_API const char *ws_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,725 @@
+// ws_capi.cu -- kernels and the extern "C" ABI declared in include/warpspeed.h.
+//
+// Launch shape: one thread per operation, grid-stride, 256-thread CTAs, grid
+// capped at 148 SMs x 8 resident CTAs.  Batch keys / values / op bytes are read
+// with coalesced streaming loads (consecutive threads own consecutive ops);
+// results are written coalesced the same way.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+#include <cub/cub.cuh>
+
+#include "warpspeed.h"
+#include "ws_kernels.cuh"
+
+using namespace ws;
+
+namespace {
+
+constexpr u32 N_STATE = 16;  // [0] tomb_ever [1] chain exhausted [2] bad keys [3] bad ops
+
+Launchers launchers_for(int design) {
+  switch (design) {
+    case D_DOUBLE: return launchers_double();
+    case D_DOUBLE_MD: return launchers_double_md();
+    case D_P2: return launchers_p2();
+    case D_P2_MD: return launchers_p2_md();
+    case D_ICEBERG: return launchers_iceberg();
+    case D_ICEBERG_MD: return launchers_iceberg_md();
+    case D_CUCKOO: return launchers_cuckoo();
+    case D_CHAINING: return launchers_chaining();
+    default: return launchers_unsafe();
+  }
+}
+
+// ------------------------------------------------------------------ kernels
+
+__global__ void k_validate(const u64* __restrict__ keys, const u8* __restrict__ ops, u64 n, u32* state) {
+  u32 bad_k = 0, bad_o = 0;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    bad_k += is_sentinel(__ldg(keys + i));
+    if (ops) {
+      const u8 o = __ldg(ops + i);
+      bad_o += ((o & 15) > OP_QUERY) | ((o >> 4) > M_MIN);
+    }
+  }
+  bad_k = __reduce_add_sync(0xFFFFFFFFu, bad_k);
+  bad_o = __reduce_add_sync(0xFFFFFFFFu, bad_o);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad_k) atomicAdd(state + 2, bad_k);
+    if (bad_o) atomicAdd(state + 3, bad_o);
+  }
+}
+
+// live pair i?  (chaining: only pair slots of allocated nodes)
+__device__ __forceinline__ bool pair_live(const Dev& d, u64 i, u64 next_node, u64& k, u64& v) {
+  if (d.design == D_CHAINING) {
+    const u64 per = (u64)d.wpn / 2, m = i / per, j = i % per;
+    if (m < 1 || m >= next_node || j >= (u64)d.bs) return false;
+  }
+  ld_cell(d.cells + 2 * i, k, v);
+  return !is_sentinel(k);
+}
+
+__global__ void k_item_flags(Dev d, u64 npairs, u64 next_node, u8* flags) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < npairs; i += (u64)gridDim.x * blockDim.x) {
+    u64 k, v;
+    flags[i] = pair_live(d, i, next_node, k, v);
+  }
+}
+
+__global__ void k_checksum(Dev d, u64 npairs, u64 next_node, u64* out) {
+  u64 cnt = 0, sk = 0, sv = 0, x = 0;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < npairs; i += (u64)gridDim.x * blockDim.x) {
+    u64 k, v;
+    if (pair_live(d, i, next_node, k, v)) {
+      cnt++;
+      sk += k;
+      sv += v;
+      x ^= mix64(k ^ mix64(v));
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+    sk += __shfl_xor_sync(0xFFFFFFFFu, sk, o);
+    sv += __shfl_xor_sync(0xFFFFFFFFu, sv, o);
+    x ^= __shfl_xor_sync(0xFFFFFFFFu, x, o);
+  }
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd((unsigned long long*)out, (unsigned long long)cnt);
+    atomicAdd((unsigned long long*)out + 1, (unsigned long long)sk);
+    atomicAdd((unsigned long long*)out + 2, (unsigned long long)sv);
+    atomicXor((unsigned long long*)out + 3, (unsigned long long)x);
+  }
+}
+
+__global__ void k_split_pairs(const ulonglong2* pairs, u64 n, u64* keys, u64* vals) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const ulonglong2 p = pairs[i];
+    if (keys) keys[i] = p.x;
+    if (vals) vals[i] = p.y;
+  }
+}
+
+__global__ void k_pair_keys(const ulonglong2* pairs, u64 n, u64* keys) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    keys[i] = pairs[i].x;
+}
+
+// sorted keys -> (key, multiplicity) for every run longer than one
+__global__ void k_dup_runs(const u64* sorted, u64 n, u64* dk, u64* dc, u64 cap, u64* ndup) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i + 1 < n; i += (u64)gridDim.x * blockDim.x) {
+    if (sorted[i] != sorted[i + 1] || (i > 0 && sorted[i - 1] == sorted[i])) continue;
+    u64 e = i + 1;
+    while (e < n && sorted[e] == sorted[i]) e++;
+    const u64 slot = atomicAdd((unsigned long long*)ndup, 1ull);
+    if (slot < cap) { dk[slot] = sorted[i]; dc[slot] = e - i; }
+  }
+}
+
+}  // namespace
+
+// ====================================================================== table
+
+struct ws_table {
+  ws_config cfg;
+  int device;
+  Dev d;
+  Launchers L;
+  bool def_bs;
+  u64 cell_words;
+  u64 lock_words;
+  u64* h_pin;  // pinned scratch (64 words)
+  cudaStream_t s_aux;
+  cudaEvent_t ev_a, ev_b;
+};
+
+namespace {
+
+inline int cuda_err(cudaError_t e) { return e == cudaSuccess ? WS_OK : WS_ERR_CUDA; }
+#define WS_CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return WS_ERR_CUDA; } while (0)
+
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+bool is_device_ptr(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+u64 next_pow2(u64 x) {
+  u64 p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+Mod make_mod(u64 d) {
+  Mod m;
+  m.d = d ? d : 1;
+  m.mask = (d && !(d & (d - 1))) ? d - 1 : 0;
+  return m;
+}
+
+// reset the invalid counters and count sentinel keys / bad op bytes
+int validate(ws_table* t, const u64* keys, const u8* ops, u64 n, cudaStream_t s, bool sync, u32 flags) {
+  if (flags & WS_F_NO_CHECK) return WS_OK;
+  WS_CK(cudaMemsetAsync(t->d.state + 2, 0, 2 * sizeof(u32), s));
+  if (n) k_validate<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(keys, ops, n, t->d.state);
+  WS_CK(cudaGetLastError());
+  if (!sync) return WS_OK;
+  WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 2, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  WS_CK(cudaStreamSynchronize(s));
+  const u32* c = (const u32*)t->h_pin;
+  if (c[0]) return WS_ERR_INVALID_KEY;
+  if (c[1]) return WS_ERR_INVALID_OP;
+  return WS_OK;
+}
+
+// chaining: grow the node pool by 1.5x when a launch exhausted it
+int chain_grow(ws_table* t, cudaStream_t s) {
+  const u64 old = t->d.chain_cap;
+  const u64 ncap = old + std::max<u64>(old / 2, 64);
+  const u64 words = ncap * (u64)t->d.wpn;
+  u64* nc = nullptr;
+  WS_CK(cudaMallocAsync((void**)&nc, words * 8, s));
+  WS_CK(cudaMemcpyAsync(nc, t->d.cells, old * t->d.wpn * 8, cudaMemcpyDeviceToDevice, s));
+  WS_CK(cudaMemsetAsync(nc + old * t->d.wpn, 0, (ncap - old) * t->d.wpn * 8, s));
+  WS_CK(cudaFreeAsync(t->d.cells, s));
+  t->d.cells = nc;
+  t->d.chain_cap = ncap;
+  t->cell_words = words;
+  // every index < old was handed out; failed bumps overshot past it
+  WS_CK(cudaMemcpyAsync(t->h_pin, t->d.chain_next, 8, cudaMemcpyDeviceToHost, s));
+  WS_CK(cudaStreamSynchronize(s));
+  if (t->h_pin[0] > old) t->h_pin[0] = old;
+  WS_CK(cudaMemcpyAsync(t->d.chain_next, t->h_pin, 8, cudaMemcpyHostToDevice, s));
+  WS_CK(cudaMemsetAsync(t->d.state + 1, 0, sizeof(u32), s));
+  WS_CK(cudaStreamSynchronize(s));
+  return WS_OK;
+}
+
+// Run one batch whose buffers are all device-resident.
+int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
+               u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
+               bool query_only) {
+  const bool sync = (flags & WS_F_SYNC_CHECK) != 0;
+  int rc = validate(t, keys, ops, n, s, sync, flags);
+  if (rc) return rc;
+  if (!n) return WS_OK;
+  const int gated = (flags & WS_F_NO_CHECK) ? 0 : 1;
+  const int conc = (has_erase || t->cfg.multi_stream) ? 1 : 0;
+  if (query_only && !(flags & WS_F_SERIAL)) {
+    QueryArgs qa{t->d, keys, n, vout, status, conc, gated, t->cfg.phased ? 1 : 0, s};
+    t->L.query(qa, t->def_bs);
+    return cuda_err(cudaGetLastError());
+  }
+  const bool chain_up = t->cfg.design == D_CHAINING && has_upsert;
+  u8* st = status;
+  if (chain_up && !st) {  // the grow-and-redo protocol needs per-op statuses
+    WS_CK(cudaMallocAsync((void**)&st, n, s));
+  }
+  OpsArgs lo{t->d, ops, uop, keys, vals, n, st, vout, nullptr, nullptr, nullptr, conc, gated, 0,
+             (flags & WS_F_SERIAL) ? 1 : 0, s};
+  t->L.ops(lo, t->def_bs);
+  rc = cuda_err(cudaGetLastError());
+  while (rc == WS_OK && chain_up) {
+    WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    WS_CK(cudaStreamSynchronize(s));
+    if (!*(const u32*)t->h_pin) break;
+    rc = chain_grow(t, s);
+    if (rc) break;
+    lo.redo = st;
+    lo.d = t->d;  // the pool moved
+    t->L.ops(lo, t->def_bs);
+    rc = cuda_err(cudaGetLastError());
+  }
+  if (st != status) cudaFreeAsync(st, s);
+  return rc;
+}
+
+// Host-buffer batches: stage through device memory.  Inputs are copied H2D in
+// full (the whole batch is validated before any mutation), then the batch runs
+// in chunks whose results stream back D2H on an auxiliary stream while the
+// next chunk computes.
+int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
+               u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
+               bool query_only) {
+  if (!n) return WS_OK;
+  const bool k_dev = is_device_ptr(keys), v_dev = is_device_ptr(vals), o_dev = is_device_ptr(ops);
+  const bool st_dev = is_device_ptr(status), vo_dev = is_device_ptr(vout);
+  char* buf = nullptr;
+  const u64 need = n * (8 * (!k_dev) + 8 * (vals && !v_dev) + (ops && !o_dev) +
+                        (status && !st_dev) + 8 * (vout && !vo_dev)) + 256;
+  WS_CK(cudaMallocAsync((void**)&buf, need, s));
+  char* p = buf;
+  auto carve = [&](u64 bytes) { char* r = p; p += (bytes + 127) & ~127ull; return r; };
+  const u64* dk = keys;
+  const u64* dv = vals;
+  const u8* dops = ops;
+  u8* dst = status;
+  u64* dvo = vout;
+  if (!k_dev) { u64* x = (u64*)carve(8 * n); WS_CK(cudaMemcpyAsync(x, keys, 8 * n, cudaMemcpyHostToDevice, s)); dk = x; }
+  if (vals && !v_dev) { u64* x = (u64*)carve(8 * n); WS_CK(cudaMemcpyAsync(x, vals, 8 * n, cudaMemcpyHostToDevice, s)); dv = x; }
+  if (ops && !o_dev) { u8* x = (u8*)carve(n); WS_CK(cudaMemcpyAsync(x, ops, n, cudaMemcpyHostToDevice, s)); dops = x; }
+  if (status && !st_dev) dst = (u8*)carve(n);
+  if (vout && !vo_dev) dvo = (u64*)carve(8 * n);
+  int rc = validate(t, dk, dops, n, s, true, flags);
+  if (rc) { cudaFreeAsync(buf, s); cudaStreamSynchronize(s); return rc; }
+  const bool chain_up = t->cfg.design == D_CHAINING && has_upsert;
+  const u64 chunk = chain_up ? n : (u64)1 << 22;
+  for (u64 off = 0; off < n && rc == WS_OK; off += chunk) {
+    const u64 m = std::min(chunk, n - off);
+    rc = run_device(t, dops ? dops + off : nullptr, uop, dk + off, dv ? dv + off : nullptr, m,
+                    dst ? dst + off : nullptr, dvo ? dvo + off : nullptr, s,
+                    WS_F_NO_CHECK | (flags & WS_F_SERIAL), has_erase,
+                    has_upsert, query_only);
+    if (rc) break;
+    if ((status && !st_dev) || (vout && !vo_dev)) {
+      WS_CK(cudaEventRecord(t->ev_a, s));
+      WS_CK(cudaStreamWaitEvent(t->s_aux, t->ev_a, 0));
+      if (status && !st_dev) WS_CK(cudaMemcpyAsync(status + off, dst + off, m, cudaMemcpyDeviceToHost, t->s_aux));
+      if (vout && !vo_dev) WS_CK(cudaMemcpyAsync(vout + off, dvo + off, 8 * m, cudaMemcpyDeviceToHost, t->s_aux));
+    }
+  }
+  WS_CK(cudaEventRecord(t->ev_b, t->s_aux));
+  WS_CK(cudaStreamWaitEvent(s, t->ev_b, 0));
+  cudaFreeAsync(buf, s);
+  WS_CK(cudaStreamSynchronize(s));
+  return rc;
+}
+
+int run_batch(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
+              u8* status, u64* vout, void* stream, u32 flags, bool has_erase, bool has_upsert,
+              bool query_only) {
+  if (!t || (!keys && n)) return WS_ERR_ARG;
+  if (cudaSetDevice(t->device) != cudaSuccess) return WS_ERR_CUDA;
+  cudaStream_t s = S(stream);
+  const bool all_dev = is_device_ptr(keys) && is_device_ptr(vals) && is_device_ptr(ops) &&
+                       is_device_ptr(status) && is_device_ptr(vout);
+  if (all_dev)
+    return run_device(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only);
+  return run_staged(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only);
+}
+
+u64 npairs_of(const ws_table* t) { return t->cell_words / 2; }
+
+int next_node_of(ws_table* t, cudaStream_t s, u64& nn) {
+  nn = 0;
+  if (t->cfg.design != D_CHAINING) return WS_OK;
+  WS_CK(cudaMemcpyAsync(t->h_pin, t->d.chain_next, 8, cudaMemcpyDeviceToHost, s));
+  WS_CK(cudaStreamSynchronize(s));
+  nn = t->h_pin[0];
+  if (nn > t->d.chain_cap) nn = t->d.chain_cap;
+  return WS_OK;
+}
+
+// live pairs compacted (in slot order) into a fresh device buffer
+int compact_items(ws_table* t, cudaStream_t s, ulonglong2** out, u64* count) {
+  u64 nn;
+  int rc = next_node_of(t, s, nn);
+  if (rc) return rc;
+  const u64 np = npairs_of(t);
+  u8* flags = nullptr;
+  ulonglong2* sel = nullptr;
+  u64* nsel = nullptr;
+  WS_CK(cudaMallocAsync((void**)&flags, np, s));
+  WS_CK(cudaMallocAsync((void**)&sel, np * sizeof(ulonglong2), s));
+  WS_CK(cudaMallocAsync((void**)&nsel, 8, s));
+  k_item_flags<<<grid_for(np), kThreads, 0, s>>>(t->d, np, nn, flags);
+  size_t tmp_bytes = 0;
+  const ulonglong2* in = (const ulonglong2*)t->d.cells;
+  cub::DeviceSelect::Flagged(nullptr, tmp_bytes, in, flags, sel, nsel, (int64_t)np, s);
+  void* tmp = nullptr;
+  WS_CK(cudaMallocAsync(&tmp, tmp_bytes + 16, s));
+  cub::DeviceSelect::Flagged(tmp, tmp_bytes, in, flags, sel, nsel, (int64_t)np, s);
+  WS_CK(cudaMemcpyAsync(t->h_pin, nsel, 8, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(flags, s);
+  cudaFreeAsync(nsel, s);
+  WS_CK(cudaStreamSynchronize(s));
+  *count = t->h_pin[0];
+  *out = sel;
+  return cuda_err(cudaGetLastError());
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+
+extern "C" {
+
+const char* ws_strerror(int code) {
+  switch (code) {
+    case WS_OK: return "ok";
+    case WS_ERR_INVALID_KEY: return "batch contains a reserved sentinel key (0, 2^64-1 or 2^64-2)";
+    case WS_ERR_CONFIG: return "invalid table configuration";
+    case WS_ERR_CUDA: return "CUDA error";
+    case WS_ERR_ALLOC: return "device allocation failed";
+    case WS_ERR_ARG: return "invalid argument";
+    case WS_ERR_INVALID_OP: return "invalid op byte (kind > 2 or merge > 4)";
+    default: return "unknown error";
+  }
+}
+
+int ws_create(const ws_config* cfg, int device, ws_table** out) {
+  if (!cfg || !out) return WS_ERR_ARG;
+  *out = nullptr;
+  const ws_config& c = *cfg;
+  if (c.design < 0 || c.design > D_UNSAFE || c.bucket_size <= 0 || c.capacity_slots == 0 ||
+      c.capacity_slots % (u64)c.bucket_size || c.n_seeds < 1 || c.line_bytes < 16 ||
+      c.ways < 2 || c.ways > 8 || c.path_depth < 1 || c.probe_cap < 1)
+    return WS_ERR_CONFIG;
+  const u64 nb = c.capacity_slots / (u64)c.bucket_size;
+  const bool ice = c.design == D_ICEBERG || c.design == D_ICEBERG_MD;
+  if (ice && (c.front_buckets < 1 || c.front_buckets >= nb)) return WS_ERR_CONFIG;
+  if (c.design == D_CHAINING && (2 * c.bucket_size + 2) * 8 > 2 * c.line_bytes) return WS_ERR_CONFIG;
+  if (cudaSetDevice(device) != cudaSuccess) return WS_ERR_CUDA;
+
+  ws_table* t = new (std::nothrow) ws_table();
+  if (!t) return WS_ERR_ALLOC;
+  t->cfg = c;
+  t->device = device;
+  t->L = launchers_for(c.design);
+  t->def_bs = c.bucket_size == default_bs(c.design);
+  Dev& d = t->d;
+  d.design = c.design;
+  d.bs = c.bucket_size;
+  d.md = c.design == D_DOUBLE_MD || c.design == D_P2_MD || c.design == D_ICEBERG_MD;
+  d.cap = c.capacity_slots;
+  d.nb = nb;
+  d.front = ice ? c.front_buckets : nb;
+  d.back = ice ? nb - c.front_buckets : 0;
+  d.nbm = make_mod(nb);
+  d.frontm = make_mod(d.front);
+  d.backm = make_mod(d.back ? d.back : 1);
+  for (int i = 0; i < 8; i++) d.seeds[i] = i < c.n_seeds ? c.seeds[i] : 0;
+  d.shortcut = c.shortcut_slots;
+  d.zcc = c.zero_count_cap;
+  d.probe_cap = c.probe_cap;
+  d.ways = c.ways;
+  d.depth = c.path_depth;
+  d.phased = c.phased;
+  d.lock_elided = c.design == D_UNSAFE;
+  d.line_bytes = c.line_bytes;
+  d.wpn = 2 * c.bucket_size + 2;
+
+  auto fail = [&](int code) { ws_destroy(t); return code; };
+  if (c.design == D_CHAINING) {
+    const u64 heads = nb + 1;
+    u64 pool = c.chain_pool_nodes ? c.chain_pool_nodes : heads + std::max<u64>(64, heads / 2);
+    if (pool < heads + 1) pool = heads + 1;
+    d.chain_cap = pool;
+    t->cell_words = pool * (u64)d.wpn;
+    if (cudaMalloc((void**)&d.chain_next, 8) != cudaSuccess) return fail(WS_ERR_ALLOC);
+  } else {
+    t->cell_words = 2 * c.capacity_slots;
+  }
+  if (cudaMalloc((void**)&d.cells, t->cell_words * 8) != cudaSuccess) return fail(WS_ERR_ALLOC);
+  if (cudaMemset(d.cells, 0, t->cell_words * 8) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (d.md) {
+    if (cudaMalloc((void**)&d.tags, c.capacity_slots * 2) != cudaSuccess) return fail(WS_ERR_ALLOC);
+    if (cudaMemset(d.tags, 0, c.capacity_slots * 2) != cudaSuccess) return fail(WS_ERR_CUDA);
+  }
+  t->lock_words = (nb + 31) / 32;
+  if (cudaMalloc((void**)&d.locks, t->lock_words * 4) != cudaSuccess) return fail(WS_ERR_ALLOC);
+  if (cudaMemset(d.locks, 0, t->lock_words * 4) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (cudaMalloc((void**)&d.state, N_STATE * 4) != cudaSuccess) return fail(WS_ERR_ALLOC);
+  if (cudaMemset(d.state, 0, N_STATE * 4) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (c.design == D_CHAINING) {
+    const u64 nn = nb + 1;
+    if (cudaMemcpy(d.chain_next, &nn, 8, cudaMemcpyHostToDevice) != cudaSuccess) return fail(WS_ERR_CUDA);
+  }
+  if (c.design == D_CUCKOO) {
+    // BFS workspace: every visited entry is a distinct bucket, and one
+    // expansion adds at most bucket_size * ways entries (cuckoo.py:107-156)
+    const u64 E = std::min<u64>(nb + 8, 8 + (u64)BFS_BUDGET * c.bucket_size * c.ways) + c.path_depth + 80;
+    const u64 SC = next_pow2(2 * E + 16);
+    d.bfs_entries = E;
+    d.bfs_seen_cap = SC;
+    d.bfs_stride = 4 * E + SC + SC / 2 + 2;
+    d.n_bfs = 64;
+    const u64 bytes = d.bfs_stride * 8 * d.n_bfs;
+    if (cudaMalloc((void**)&d.bfs_mem, bytes) != cudaSuccess) return fail(WS_ERR_ALLOC);
+    if (cudaMemset(d.bfs_mem, 0, bytes) != cudaSuccess) return fail(WS_ERR_CUDA);
+    if (cudaMalloc((void**)&d.bfs_busy, 4 * d.n_bfs) != cudaSuccess) return fail(WS_ERR_ALLOC);
+    if (cudaMemset(d.bfs_busy, 0, 4 * d.n_bfs) != cudaSuccess) return fail(WS_ERR_CUDA);
+  }
+  if (cudaMallocHost((void**)&t->h_pin, 64 * 8) != cudaSuccess) return fail(WS_ERR_ALLOC);
+  if (cudaStreamCreateWithFlags(&t->s_aux, cudaStreamNonBlocking) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&t->ev_a, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&t->ev_b, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(WS_ERR_CUDA);
+  *out = t;
+  return WS_OK;
+}
+
+int ws_destroy(ws_table* t) {
+  if (!t) return WS_OK;
+  cudaSetDevice(t->device);
+  cudaDeviceSynchronize();
+  Dev& d = t->d;
+  if (d.cells) cudaFree(d.cells);
+  if (d.tags) cudaFree(d.tags);
+  if (d.locks) cudaFree(d.locks);
+  if (d.state) cudaFree(d.state);
+  if (d.chain_next) cudaFree(d.chain_next);
+  if (d.bfs_mem) cudaFree(d.bfs_mem);
+  if (d.bfs_busy) cudaFree(d.bfs_busy);
+  if (t->h_pin) cudaFreeHost(t->h_pin);
+  if (t->s_aux) cudaStreamDestroy(t->s_aux);
+  if (t->ev_a) cudaEventDestroy(t->ev_a);
+  if (t->ev_b) cudaEventDestroy(t->ev_b);
+  delete t;
+  return WS_OK;
+}
+
+int ws_clear(ws_table* t, void* stream) {
+  if (!t) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  cudaStream_t s = S(stream);
+  Dev& d = t->d;
+  WS_CK(cudaMemsetAsync(d.cells, 0, t->cell_words * 8, s));
+  if (d.tags) WS_CK(cudaMemsetAsync(d.tags, 0, d.cap * 2, s));
+  WS_CK(cudaMemsetAsync(d.locks, 0, t->lock_words * 4, s));
+  WS_CK(cudaMemsetAsync(d.state, 0, N_STATE * 4, s));
+  if (t->cfg.design == D_CHAINING) {
+    t->h_pin[0] = d.nb + 1;
+    WS_CK(cudaMemcpyAsync(d.chain_next, t->h_pin, 8, cudaMemcpyHostToDevice, s));
+    WS_CK(cudaStreamSynchronize(s));
+  }
+  return WS_OK;
+}
+
+int ws_upsert(ws_table* t, const uint64_t* keys, const uint64_t* vals, uint64_t n, uint32_t merge,
+              uint8_t* status, void* stream, uint32_t flags) {
+  if (merge > WS_MERGE_MIN || (!vals && n)) return WS_ERR_ARG;
+  return run_batch(t, nullptr, (u8)(OP_UPSERT | (merge << 4)), (const u64*)keys, (const u64*)vals, n,
+                   status, nullptr, stream, flags, false, true, false);
+}
+
+int ws_query(ws_table* t, const uint64_t* keys, uint64_t n, uint64_t* vals_out, uint8_t* found,
+             void* stream, uint32_t flags) {
+  return run_batch(t, nullptr, OP_QUERY, (const u64*)keys, nullptr, n, found, (u64*)vals_out, stream,
+                   flags, false, false, true);
+}
+
+int ws_erase(ws_table* t, const uint64_t* keys, uint64_t n, uint8_t* found, void* stream,
+             uint32_t flags) {
+  return run_batch(t, nullptr, OP_ERASE, (const u64*)keys, nullptr, n, found, nullptr, stream, flags,
+                   true, false, false);
+}
+
+int ws_mixed(ws_table* t, const uint8_t* ops, const uint64_t* keys, const uint64_t* vals, uint64_t n,
+             uint8_t* status, uint64_t* vals_out, void* stream, uint32_t flags) {
+  if (!ops && n) return WS_ERR_ARG;
+  // a zero-filled value array is substituted when none is given
+  return run_batch(t, ops, 0, (const u64*)keys, (const u64*)vals, n, status, (u64*)vals_out, stream,
+                   flags, true, true, false);
+}
+
+int ws_locate(ws_table* t, const uint64_t* keys, uint64_t n, int64_t* slot_out, void* stream) {
+  if (!t || (!keys && n) || (!slot_out && n)) return WS_ERR_ARG;
+  if (!n) return WS_OK;
+  cudaSetDevice(t->device);
+  cudaStream_t s = S(stream);
+  const bool kd = is_device_ptr(keys), od = is_device_ptr(slot_out);
+  u64* dk = (u64*)keys;
+  i64* dout = (i64*)slot_out;
+  if (!kd) { WS_CK(cudaMallocAsync((void**)&dk, 8 * n, s)); WS_CK(cudaMemcpyAsync(dk, keys, 8 * n, cudaMemcpyHostToDevice, s)); }
+  if (!od) WS_CK(cudaMallocAsync((void**)&dout, 8 * n, s));
+  LocateArgs la{t->d, dk, n, dout, s};
+  t->L.locate(la, t->def_bs);
+  int rc = cuda_err(cudaGetLastError());
+  if (!od) WS_CK(cudaMemcpyAsync(slot_out, dout, 8 * n, cudaMemcpyDeviceToHost, s));
+  if (!kd) cudaFreeAsync(dk, s);
+  if (!od) cudaFreeAsync(dout, s);
+  WS_CK(cudaStreamSynchronize(s));
+  return rc;
+}
+
+int ws_probe_counts(ws_table* t, const uint8_t* ops, const uint64_t* keys, const uint64_t* vals,
+                    uint64_t n, uint8_t* status, uint64_t* vals_out, uint32_t* probes,
+                    uint64_t* lock_touches, void* stream, uint32_t flags) {
+  if (!t || !ops || !keys || !probes) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  cudaStream_t s = S(stream);
+  if (!n) { if (lock_touches) *lock_touches = 0; return WS_OK; }
+  // stage everything (instrumented runs are measurement passes, not hot)
+  char* buf = nullptr;
+  const u64 need = n * (1 + 8 + 8 + 1 + 8 + 4) + 1024;
+  WS_CK(cudaMallocAsync((void**)&buf, need, s));
+  char* p = buf;
+  auto carve = [&](u64 bytes) { char* r = p; p += (bytes + 127) & ~127ull; return r; };
+  u8* dops = (u8*)carve(n);
+  u64* dk = (u64*)carve(8 * n);
+  u64* dv = (u64*)carve(8 * n);
+  u8* dst = (u8*)carve(n);
+  u64* dvo = (u64*)carve(8 * n);
+  u32* dpr = (u32*)carve(4 * n);
+  u64* dlock = (u64*)carve(8);
+  WS_CK(cudaMemcpyAsync(dops, ops, n, cudaMemcpyDefault, s));
+  WS_CK(cudaMemcpyAsync(dk, keys, 8 * n, cudaMemcpyDefault, s));
+  if (vals) WS_CK(cudaMemcpyAsync(dv, vals, 8 * n, cudaMemcpyDefault, s));
+  else WS_CK(cudaMemsetAsync(dv, 0, 8 * n, s));
+  WS_CK(cudaMemsetAsync(dlock, 0, 8, s));
+  int rc = validate(t, dk, dops, n, s, true, 0);
+  if (rc) { cudaFreeAsync(buf, s); cudaStreamSynchronize(s); return rc; }
+  OpsArgs lo{t->d, dops, 0, dk, dv, n, dst, dvo, nullptr, dpr, dlock, 1, 0, 1,
+             (flags & WS_F_SERIAL) ? 1 : 0, s};
+  t->L.ops(lo, t->def_bs);
+  rc = cuda_err(cudaGetLastError());
+  if (!rc && status) WS_CK(cudaMemcpyAsync(status, dst, n, cudaMemcpyDefault, s));
+  if (!rc && vals_out) WS_CK(cudaMemcpyAsync(vals_out, dvo, 8 * n, cudaMemcpyDefault, s));
+  if (!rc) WS_CK(cudaMemcpyAsync(probes, dpr, 4 * n, cudaMemcpyDefault, s));
+  if (!rc) WS_CK(cudaMemcpyAsync(t->h_pin, dlock, 8, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(buf, s);
+  WS_CK(cudaStreamSynchronize(s));
+  if (!rc && lock_touches) *lock_touches = t->h_pin[0];
+  return rc;
+}
+
+int ws_occupied(ws_table* t, uint64_t* count_out, void* stream) {
+  uint64_t cs[4];
+  int rc = ws_checksum(t, cs, stream);
+  if (!rc && count_out) *count_out = cs[0];
+  return rc;
+}
+
+int ws_checksum(ws_table* t, uint64_t out[4], void* stream) {
+  if (!t || !out) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  cudaStream_t s = S(stream);
+  u64 nn;
+  int rc = next_node_of(t, s, nn);
+  if (rc) return rc;
+  u64* dout = nullptr;
+  WS_CK(cudaMallocAsync((void**)&dout, 32, s));
+  WS_CK(cudaMemsetAsync(dout, 0, 32, s));
+  const u64 np = npairs_of(t);
+  k_checksum<<<grid_for(np), kThreads, 0, s>>>(t->d, np, nn, dout);
+  WS_CK(cudaMemcpyAsync(t->h_pin, dout, 32, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(dout, s);
+  WS_CK(cudaStreamSynchronize(s));
+  memcpy(out, t->h_pin, 32);
+  return cuda_err(cudaGetLastError());
+}
+
+int ws_export_items(ws_table* t, uint64_t* keys, uint64_t* vals, uint64_t cap, uint64_t* n_out,
+                    void* stream) {
+  if (!t) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  cudaStream_t s = S(stream);
+  ulonglong2* sel = nullptr;
+  u64 cnt = 0;
+  int rc = compact_items(t, s, &sel, &cnt);
+  if (rc) return rc;
+  if (n_out) *n_out = cnt;
+  const u64 m = std::min<u64>(cap, cnt);
+  if (m && (keys || vals)) {
+    u64* tmp = nullptr;
+    WS_CK(cudaMallocAsync((void**)&tmp, 16 * m, s));
+    k_split_pairs<<<grid_for(m), kThreads, 0, s>>>(sel, m, keys ? tmp : nullptr, vals ? tmp + m : nullptr);
+    if (keys) WS_CK(cudaMemcpyAsync(keys, tmp, 8 * m, cudaMemcpyDefault, s));
+    if (vals) WS_CK(cudaMemcpyAsync(vals, tmp + m, 8 * m, cudaMemcpyDefault, s));
+    cudaFreeAsync(tmp, s);
+  }
+  cudaFreeAsync(sel, s);
+  WS_CK(cudaStreamSynchronize(s));
+  return cuda_err(cudaGetLastError());
+}
+
+int ws_duplicate_scan(ws_table* t, uint64_t* dup_keys, uint64_t* dup_counts, uint64_t cap,
+                      uint64_t* n_dup_out, void* stream) {
+  if (!t) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  cudaStream_t s = S(stream);
+  ulonglong2* sel = nullptr;
+  u64 cnt = 0;
+  int rc = compact_items(t, s, &sel, &cnt);
+  if (rc) return rc;
+  u64 ndup = 0;
+  if (cnt > 1) {
+    u64 *k_in = nullptr, *k_out = nullptr, *dk = nullptr, *dc = nullptr, *dn = nullptr;
+    const u64 cap_d = std::max<u64>(cap, 1);
+    WS_CK(cudaMallocAsync((void**)&k_in, 8 * cnt, s));
+    WS_CK(cudaMallocAsync((void**)&k_out, 8 * cnt, s));
+    WS_CK(cudaMallocAsync((void**)&dk, 8 * cap_d, s));
+    WS_CK(cudaMallocAsync((void**)&dc, 8 * cap_d, s));
+    WS_CK(cudaMallocAsync((void**)&dn, 8, s));
+    WS_CK(cudaMemsetAsync(dn, 0, 8, s));
+    k_pair_keys<<<grid_for(cnt), kThreads, 0, s>>>(sel, cnt, k_in);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, k_in, k_out, (int64_t)cnt, 0, 64, s);
+    void* tmp = nullptr;
+    WS_CK(cudaMallocAsync(&tmp, tb + 16, s));
+    cub::DeviceRadixSort::SortKeys(tmp, tb, k_in, k_out, (int64_t)cnt, 0, 64, s);
+    k_dup_runs<<<grid_for(cnt), kThreads, 0, s>>>(k_out, cnt, dk, dc, cap_d, dn);
+    WS_CK(cudaMemcpyAsync(t->h_pin, dn, 8, cudaMemcpyDeviceToHost, s));
+    WS_CK(cudaStreamSynchronize(s));
+    ndup = t->h_pin[0];
+    const u64 m = std::min<u64>(ndup, cap);
+    if (m && dup_keys) WS_CK(cudaMemcpyAsync(dup_keys, dk, 8 * m, cudaMemcpyDefault, s));
+    if (m && dup_counts) WS_CK(cudaMemcpyAsync(dup_counts, dc, 8 * m, cudaMemcpyDefault, s));
+    cudaFreeAsync(tmp, s);
+    cudaFreeAsync(k_in, s);
+    cudaFreeAsync(k_out, s);
+    cudaFreeAsync(dk, s);
+    cudaFreeAsync(dc, s);
+    cudaFreeAsync(dn, s);
+  }
+  cudaFreeAsync(sel, s);
+  WS_CK(cudaStreamSynchronize(s));
+  if (n_dup_out) *n_dup_out = ndup;
+  return cuda_err(cudaGetLastError());
+}
+
+int ws_export_raw(ws_table* t, uint64_t* words, uint64_t nwords, uint16_t* tags, void* stream) {
+  if (!t) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  cudaStream_t s = S(stream);
+  const u64 m = std::min<u64>(nwords, t->cell_words);
+  if (words && m) WS_CK(cudaMemcpyAsync(words, t->d.cells, 8 * m, cudaMemcpyDefault, s));
+  if (tags) {
+    if (t->d.tags) WS_CK(cudaMemcpyAsync(tags, t->d.tags, 2 * t->d.cap, cudaMemcpyDefault, s));
+    else WS_CK(cudaMemsetAsync(tags, 0, 0, s));
+  }
+  WS_CK(cudaStreamSynchronize(s));
+  return WS_OK;
+}
+
+int ws_info(ws_table* t, ws_info_t* info) {
+  if (!t || !info) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  memset(info, 0, sizeof(*info));
+  info->capacity_slots = t->d.cap;
+  info->num_buckets = t->d.nb;
+  info->primary_buckets = t->d.front;
+  info->lock_bytes = t->lock_words * 4;
+  info->device = t->device;
+  if (t->cfg.design == D_CHAINING) {
+    info->node_bytes = t->cell_words * 8;
+    info->pool_nodes = t->d.chain_cap;
+  } else {
+    info->slot_bytes = t->cell_words * 8;
+  }
+  info->tag_bytes = t->d.tags ? t->d.cap * 2 : 0;
+  u32 st[2] = {0, 0};
+  WS_CK(cudaMemcpy(st, t->d.state, 8, cudaMemcpyDeviceToHost));
+  info->tombstones_ever = (int32_t)st[0];
+  if (t->cfg.design == D_CHAINING) {
+    u64 nn = 0;
+    WS_CK(cudaMemcpy(&nn, t->d.chain_next, 8, cudaMemcpyDeviceToHost));
+    info->next_node = std::min<u64>(nn, t->d.chain_cap);
+  }
+  return WS_OK;
+}
+
+}  // extern "C"

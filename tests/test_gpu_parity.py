@@ -1,0 +1,290 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the oracle.
+
+1. Serial replay of every reference golden stream on the device (one device
+   thread, index order): statuses, values, probe counts, lock touches, slot
+   layout, tags and chaining node numbering must equal the reference's --
+   bit for bit.
+2. Concurrent batches (one thread per op) against the oracle on identical
+   inputs: same hit/miss set and values, same final key->value map, zero
+   duplicates, zero FULL at the tested loads.
+3. Full-size (2^28-slot) P2-MD fill through size-independent properties.
+"""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, cfg_for
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+FIXTURES = sorted(glob.glob(os.path.join(GOLDEN, "ops_*.npz")))
+U64 = (1 << 64) - 1
+
+
+def _fixture(path):
+    from paper_2509_16407_b200.core import TableConfig
+    z = np.load(path)
+    name = os.path.basename(path)[4:-4]
+    design = name.rsplit("_", 1)[0]
+    extra = json.loads(str(z["extra"][0]))
+    cfg = TableConfig(design=design, capacity_slots=int(z["capacity"][0]),
+                      seed=int(z["seed"][0]), **extra)
+    return z, cfg
+
+
+def _oracle(cfg):
+    from oracle import OracleTable
+    return OracleTable(cfg)
+
+
+def _table(cfg, **kw):
+    from paper_2509_16407_b200 import make_table
+    return make_table(cfg, **kw)
+
+
+# ------------------------------------------------------------------ 1. serial
+
+@pytest.mark.parametrize("path", FIXTURES, ids=lambda p: os.path.basename(p)[4:-4])
+def test_serial_replay_matches_reference(path):
+    z, cfg = _fixture(path)
+    t = _table(cfg)
+    st, vo, probes, locks = t.probe_batch(z["ops"], z["keys"], z["vals"], serial=True)
+    np.testing.assert_array_equal(st, z["status"])
+    np.testing.assert_array_equal(vo, z["qvals"])
+    np.testing.assert_array_equal(probes, z["probes"])
+    assert locks == int(z["lock_touches"][0])
+    k, v = t.items_arrays()
+    np.testing.assert_array_equal(k, z["item_keys"])
+    np.testing.assert_array_equal(v, z["item_vals"])
+    words, tags = t._raw()
+    if cfg.design == "chaining":
+        assert t.arena.next_node == int(z["next_node"][0])
+        assert t.arena.capacity_nodes == int(z["arena_capacity"][0])
+        ref = z["words"].reshape(-1, 16)
+        got = words[: ref.size].reshape(-1, 16)
+        np.testing.assert_array_equal(got[:, :14:2], ref[:, :14:2])
+        np.testing.assert_array_equal(got[:, 14], ref[:, 14])
+    else:
+        np.testing.assert_array_equal(words[0::2], z["slot_keys"])
+        if "tags" in z.files:
+            np.testing.assert_array_equal(tags, z["tags"])
+    assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("path", FIXTURES[::4], ids=lambda p: os.path.basename(p)[4:-4])
+def test_serial_mixed_without_instrumentation(path):
+    z, cfg = _fixture(path)
+    t = _table(cfg)
+    st, vo = t.mixed_batch(z["ops"], z["keys"], z["vals"], serial=True)
+    np.testing.assert_array_equal(st.numpy(), z["status"])
+    np.testing.assert_array_equal(vo.numpy(), z["qvals"])
+
+
+@pytest.mark.parametrize("design", ["p2_md", "double", "iceberg_md", "cuckoo", "chaining"])
+def test_scalar_api_follows_reference_stream(design):
+    from paper_2509_16407_b200.tables import UpsertStatus
+    path = os.path.join(GOLDEN, f"ops_{design}_mixed.npz")
+    z, cfg = _fixture(path)
+    t = _table(cfg)
+    names = [None, "keep", "add", "max", "min"]
+    status = {UpsertStatus.INSERTED: 0, UpsertStatus.UPDATED: 1, UpsertStatus.FULL: 2}
+    for i in range(600):
+        op, key, val = int(z["ops"][i]), int(z["keys"][i]), int(z["vals"][i])
+        kind, m = op & 15, op >> 4
+        if kind == 0:
+            assert status[t.upsert(key, val, names[m])] == z["status"][i]
+        elif kind == 1:
+            assert int(t.erase(key)) == z["status"][i]
+        else:
+            got = t.query(key)
+            assert (got is not None) == bool(z["status"][i])
+            if got is not None:
+                assert got == int(z["qvals"][i])
+
+
+# -------------------------------------------------------------- 2. concurrent
+
+def _keys(seed, n):
+    from paper_2509_16407_b200.workload import gen_uniform_keys
+    return gen_uniform_keys(seed, n)
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda().view(torch.uint64)
+
+
+def _np(t):
+    return t.cpu().view(torch.int64).numpy().view(np.uint64) if t.dtype == torch.uint64 else t.cpu().numpy()
+
+
+LOADS = {"double": 0.85, "double_md": 0.85, "p2": 0.9, "p2_md": 0.9, "iceberg": 0.9,
+         "iceberg_md": 0.9, "cuckoo": 0.9, "chaining": 1.5, "unsafe_reference": 0.9}
+
+
+@pytest.mark.parametrize("design", list(LOADS))
+def test_concurrent_fill_then_query_matches_oracle(design):
+    cap = 1 << 16
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * 4096, seed=42)
+    t = _table(cfg)
+    o = _oracle(cfg)
+    n = int(t.capacity_slots * LOADS[design])
+    keys = _keys(42, n)
+    vals = keys & np.uint64(0xFFFF)
+    for part in np.array_split(np.arange(n), 4):
+        st = _np(t.upsert_batch(_cuda(keys[part]), _cuda(vals[part])))
+        assert (st == 0).all(), np.bincount(st)
+    o.upsert_batch(keys, vals)
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
+    miss = _keys(7, n // 2)
+    q = np.concatenate([keys[::2], miss])
+    found, got = t.query_batch(_cuda(q))
+    ofound, oval = o.query_batch(q)
+    np.testing.assert_array_equal(_np(found).astype(bool), ofound)
+    np.testing.assert_array_equal(_np(got), oval)
+
+
+@pytest.mark.parametrize("design", ["p2_md", "p2", "double_md", "iceberg_md", "cuckoo", "chaining"])
+def test_concurrent_upsert_add_with_duplicate_keys(design):
+    from paper_2509_16407_b200.workload import zipf_ranks
+    cap = 1 << 15
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * 2048, seed=5)
+    t = _table(cfg)
+    universe = _keys(11, int(t.capacity_slots * 0.6))
+    ranks = zipf_ranks(len(universe), 200_000, 0.99, seed=3) - 1
+    keys = universe[ranks]
+    vals = (np.arange(len(keys), dtype=np.uint64) * np.uint64(2654435761)) & np.uint64(0xFFFFFF)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals), merge="add"))
+    assert (st != 2).all()
+    u, inv = np.unique(keys, return_inverse=True)
+    want = np.zeros(len(u), dtype=np.uint64)
+    np.add.at(want, inv, vals)
+    assert dict(t.items()) == dict(zip(u.tolist(), want.tolist()))
+    assert int((st == 0).sum()) == len(u)  # exactly one INSERTED per distinct key
+    assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("design", ["p2_md", "double", "iceberg_md", "iceberg", "cuckoo", "chaining"])
+def test_concurrent_aging_mixed_batch(design):
+    """Aging-style batch (reference runners.py:298-306): insert new, erase
+    oldest, query present, query absent -- roles key-disjoint."""
+    from paper_2509_16407_b200.tables import OP_ERASE, OP_QUERY, OP_UPSERT
+    cap = 1 << 15
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * 4096, seed=9)
+    t = _table(cfg)
+    o = _oracle(cfg)
+    fill = int(t.capacity_slots * 0.85)
+    stream = _keys(3, fill + 40_000)
+    neg = _keys(4, 40_000)
+    t.upsert_batch(_cuda(stream[:fill]), _cuda(stream[:fill] & np.uint64(0xFFFF)))
+    o.upsert_batch(stream[:fill], stream[:fill] & np.uint64(0xFFFF))
+    head, nxt, sl = 0, fill, 3000
+    for it in range(6):
+        new = stream[nxt:nxt + sl]
+        old = stream[head:head + sl]
+        pos = stream[head + sl:head + 2 * sl]
+        ng = neg[it * sl:(it + 1) * sl]
+        ops = np.concatenate([np.full(sl, OP_UPSERT | (2 << 4)), np.full(sl, OP_ERASE),
+                              np.full(sl, OP_QUERY), np.full(sl, OP_QUERY)]).astype(np.uint8)
+        keys = np.concatenate([new, old, pos, ng])
+        vals = keys & np.uint64(0xFFFF)
+        perm = np.argsort((keys * np.uint64(0x9E3779B97F4A7C15)) & np.uint64(0xFFFFFFFF), kind="stable")
+        ops, keys, vals = ops[perm], keys[perm], vals[perm]
+        st, vo = t.mixed_batch(_cuda(ops), _cuda(keys), _cuda(vals))
+        ost, ovo = o.mixed_batch(ops, keys, vals)
+        np.testing.assert_array_equal(_np(st), ost)
+        np.testing.assert_array_equal(_np(vo), ovo)
+        head += sl
+        nxt += sl
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
+
+
+def test_sentinel_batch_rejected_table_untouched(design):
+    from paper_2509_16407_b200 import InvalidKeyError
+    cfg = cfg_for(design, 1 << 12)
+    t = _table(cfg)
+    t.upsert(5, 5)
+    before = t.checksum()
+    for bad in (0, U64, U64 - 1):
+        keys = np.array([7, 8, bad, 9], dtype=np.uint64)
+        with pytest.raises(InvalidKeyError):
+            t.upsert_batch(_cuda(keys), _cuda(keys))
+        with pytest.raises(InvalidKeyError):
+            t.erase_batch(_cuda(np.array([5, bad], dtype=np.uint64)))
+        with pytest.raises(InvalidKeyError):
+            t.query_batch(_cuda(keys))
+        with pytest.raises(InvalidKeyError):
+            t.upsert(bad, 1)
+    assert t.checksum() == before
+    assert dict(t.items()) == {5: 5}
+
+
+def test_host_buffers_roundtrip_through_cabi():
+    """The C ABI accepts host arrays and stages them (the FFI caller's path)."""
+    cfg = cfg_for("p2_md", 1 << 16, seed=1)
+    t = _table(cfg)
+    keys = _keys(1, 50_000)
+    st = t.upsert_batch(keys, keys ^ np.uint64(77))
+    assert not st.is_cuda and (st.numpy() == 0).all()
+    found, vals = t.query_batch(np.concatenate([keys, _keys(2, 100)]))
+    f = found.numpy()
+    assert f[:50_000].all() and not f[50_000:].any()
+    np.testing.assert_array_equal(_np(vals)[:50_000], keys ^ np.uint64(77))
+
+
+def test_chaining_grows_past_nominal_capacity():
+    cfg = cfg_for("chaining", 7 * 64, seed=1)
+    t = _table(cfg)
+    keys = _keys(5, 7 * 64 * 7)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(keys)))
+    assert (st == 0).all()
+    found, vals = t.query_batch(_cuda(keys))
+    assert _np(found).all()
+    np.testing.assert_array_equal(_np(vals), keys)
+
+
+def test_unsafe_reference_still_correct_without_races():
+    cfg = cfg_for("unsafe_reference", 1 << 14, seed=2)
+    t = _table(cfg)
+    keys = _keys(8, 10_000)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(keys)))
+    assert (st == 0).all()
+    assert t.duplicate_scan() == {}
+
+
+# ------------------------------------------------------------ 3. full size
+
+def test_p2md_2pow28_fill_and_query_properties():
+    """BASELINE config 2 at full size: 2^28 slots, insert to 0.9, then 50/50
+    queries.  Checked through size-independent properties: every insert
+    INSERTED, occupied == n, checksum (sum keys, sum values, xor-digest)
+    equal to numpy's over the inputs, all hits found with their values, no
+    miss found, no duplicates."""
+    from paper_2509_16407_b200.core import TableConfig
+    from paper_2509_16407_b200.workload import mix64_np
+    cap = 1 << 28
+    t = _table(TableConfig(design="p2_md", capacity_slots=cap, seed=42))
+    n = int(cap * 0.9)
+    keys = _keys(42, n)
+    vals = keys & np.uint64(0xFFFF)
+    dk, dv = _cuda(keys), _cuda(vals)
+    st = t.upsert_batch(dk, dv)
+    assert int((st != 0).sum()) == 0
+    with np.errstate(over="ignore"):
+        want = (n, int(keys.sum(dtype=np.uint64)), int(vals.sum(dtype=np.uint64)),
+                int(np.bitwise_xor.reduce(mix64_np(keys ^ mix64_np(vals)))))
+    assert t.checksum() == want
+    found, got = t.query_batch(dk)
+    assert bool(found.all())
+    assert torch.equal(got.view(torch.int64), dv.view(torch.int64))
+    miss = _cuda(_keys(43, 1 << 24))
+    found, _ = t.query_batch(miss)
+    assert int(found.sum()) == 0
+    assert t.duplicate_count() == 0
