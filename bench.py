@@ -204,8 +204,9 @@ def run_ours(args, rank, world):
 
     keys = dev_u64(keys_h)
     vals = dev_u64(vals_h)
-    q = torch.cat([keys[: n // 2], dev_u64(miss_h)])
+    q = torch.cat([keys[: n // 2], dev_u64(miss_h)]).view(torch.int64)  # torch lacks uint64 indexing
     q = q[torch.randperm(n, device=dev, generator=torch.Generator(device=dev).manual_seed(1))]
+    q = q.view(torch.uint64)
     stream = torch.cuda.current_stream(dev)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <new>
 
@@ -140,8 +141,16 @@ struct ws_table {
 
 namespace {
 
-inline int cuda_err(cudaError_t e) { return e == cudaSuccess ? WS_OK : WS_ERR_CUDA; }
-#define WS_CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return WS_ERR_CUDA; } while (0)
+thread_local char g_cuda_msg[256] = "CUDA error";
+
+inline int note_cuda(cudaError_t e, int line) {
+  snprintf(g_cuda_msg, sizeof g_cuda_msg, "CUDA error %s (%s) at ws_capi.cu:%d", cudaGetErrorName(e),
+           cudaGetErrorString(e), line);
+  return WS_ERR_CUDA;
+}
+inline int cuda_err_at(cudaError_t e, int line) { return e == cudaSuccess ? WS_OK : note_cuda(e, line); }
+#define cuda_err(x) cuda_err_at((x), __LINE__)
+#define WS_CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return note_cuda(e_, __LINE__); } while (0)
 
 inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
@@ -361,7 +370,7 @@ const char* ws_strerror(int code) {
     case WS_OK: return "ok";
     case WS_ERR_INVALID_KEY: return "batch contains a reserved sentinel key (0, 2^64-1 or 2^64-2)";
     case WS_ERR_CONFIG: return "invalid table configuration";
-    case WS_ERR_CUDA: return "CUDA error";
+    case WS_ERR_CUDA: return g_cuda_msg;
     case WS_ERR_ALLOC: return "device allocation failed";
     case WS_ERR_ARG: return "invalid argument";
     case WS_ERR_INVALID_OP: return "invalid op byte (kind > 2 or merge > 4)";

@@ -116,7 +116,10 @@ def _keys(seed, n):
 
 
 def _cuda(a):
-    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda().view(torch.uint64)
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint8:
+        return torch.from_numpy(a).cuda()
+    return torch.from_numpy(a.astype(np.uint64, copy=False).view(np.int64)).cuda().view(torch.uint64)
 
 
 def _np(t):
