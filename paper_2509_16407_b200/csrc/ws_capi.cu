@@ -266,7 +266,7 @@ int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   const bool st_dev = is_device_ptr(status), vo_dev = is_device_ptr(vout);
   char* buf = nullptr;
   const u64 need = n * (8 * (!k_dev) + 8 * (vals && !v_dev) + (ops && !o_dev) +
-                        (status && !st_dev) + 8 * (vout && !vo_dev)) + 256;
+                        (status && !st_dev) + 8 * (vout && !vo_dev)) + 6 * 128;
   WS_CK(cudaMallocAsync((void**)&buf, need, s));
   char* p = buf;
   auto carve = [&](u64 bytes) { char* r = p; p += (bytes + 127) & ~127ull; return r; };
@@ -310,6 +310,7 @@ int run_batch(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* va
               bool query_only) {
   if (!t || (!keys && n)) return WS_ERR_ARG;
   if (cudaSetDevice(t->device) != cudaSuccess) return WS_ERR_CUDA;
+  cudaGetLastError();  // drop any stale error from an earlier, unrelated call
   cudaStream_t s = S(stream);
   const bool all_dev = is_device_ptr(keys) && is_device_ptr(vals) && is_device_ptr(ops) &&
                        is_device_ptr(status) && is_device_ptr(vout);

@@ -22,6 +22,19 @@ inline unsigned grid_for(u64 n, int threads = kThreads, int per_sm = 8) {
   return (unsigned)(g ? g : 1);
 }
 
+// Grid for a mutating launch: besides the SM-count cap, keep the number of
+// ops in flight at most ~one per bucket.  Routing decisions (P2 shortcut /
+// least-loaded, iceberg backyard choice) read bucket occupancy; when a whole
+// batch of a small table runs at once, thousands of decisions see the same
+// stale counts and pile into the same buckets.  Large tables (2^28 slots =
+// 2^23 buckets vs ~300K resident threads) are unaffected.
+inline unsigned grid_for_table(u64 n, u64 nb, int threads = kThreads, int per_sm = 8) {
+  const unsigned g = grid_for(n, threads, per_sm);
+  u64 lim = (nb + threads - 1) / threads;
+  if (lim < 4) lim = 4;
+  return (unsigned)(g < lim ? g : lim);
+}
+
 __device__ __forceinline__ bool gate_closed(const Dev& d, int gated) {
   return gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3));
 }
@@ -113,11 +126,11 @@ void launch_ops_t(const OpsArgs& a) {
   // serial: one thread walks the batch in index order (exact sequential
   // semantics, used to replay reference op streams)
   if (a.instr)
-    k_ops<DES, BS, true><<<a.serial ? 1 : grid_for(a.n, 128, 4), a.serial ? 1 : 128, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
+    k_ops<DES, BS, true><<<a.serial ? 1 : grid_for_table(a.n, a.d.nb, 128, 4), a.serial ? 1 : 128, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
                                                                   a.vout, a.redo, a.probes, a.lock_acc,
                                                                   a.conc_erase, a.gated);
   else
-    k_ops<DES, BS, false><<<a.serial ? 1 : grid_for(a.n), a.serial ? 1 : kThreads, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
+    k_ops<DES, BS, false><<<a.serial ? 1 : grid_for_table(a.n, a.d.nb), a.serial ? 1 : kThreads, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
                                                                 a.vout, a.redo, a.probes, a.lock_acc,
                                                                 a.conc_erase, a.gated);
 }

@@ -184,11 +184,13 @@ def test_concurrent_aging_mixed_batch(design):
     o = _oracle(cfg)
     fill = int(t.capacity_slots * 0.85)
     stream = _keys(3, fill + 40_000)
-    neg = _keys(4, 40_000)
+    neg = _keys(4, 40_000)  # 12 slices x 1000
     t.upsert_batch(_cuda(stream[:fill]), _cuda(stream[:fill] & np.uint64(0xFFFF)))
     o.upsert_batch(stream[:fill], stream[:fill] & np.uint64(0xFFFF))
-    head, nxt, sl = 0, fill, 3000
-    for it in range(6):
+    # 1000-op slices (~3.5% of the fill; the reference ages in 1% slices) keep
+    # the sequential oracle itself free of order-dependent FULLs
+    head, nxt, sl = 0, fill, 1000
+    for it in range(12):
         new = stream[nxt:nxt + sl]
         old = stream[head:head + sl]
         pos = stream[head + sl:head + 2 * sl]
@@ -201,8 +203,9 @@ def test_concurrent_aging_mixed_batch(design):
         ops, keys, vals = ops[perm], keys[perm], vals[perm]
         st, vo = t.mixed_batch(_cuda(ops), _cuda(keys), _cuda(vals))
         ost, ovo = o.mixed_batch(ops, keys, vals)
-        np.testing.assert_array_equal(_np(st), ost)
-        np.testing.assert_array_equal(_np(vo), ovo)
+        assert not ((ost == 2) & ((ops & 15) == OP_UPSERT)).any(), "ill-posed: oracle hit FULL"
+        bad = np.nonzero((_np(st) != ost) | (_np(vo) != ovo))[0]
+        assert bad.size == 0, (it, [(int(ops[i]), int(_np(st)[i]), int(ost[i])) for i in bad[:10]])
         head += sl
         nxt += sl
     assert dict(t.items()) == o.as_dict()
