@@ -178,6 +178,10 @@ __device__ __forceinline__ void lock_bucket(u32* locks, u64 b) {
 __device__ __forceinline__ void unlock_bucket(u32* locks, u64 b) {
   red_and_release(locks + (b >> 5), ~(1u << (b & 31)));
 }
+__device__ __forceinline__ bool try_lock_bucket(u32* locks, u64 b) {
+  const u32 bit = 1u << (b & 31);
+  return !(atom_or_acquire(locks + (b >> 5), bit) & bit);
+}
 
 // ------------------------------------------------------ probe accounting
 // Distinct line-sized regions touched by one op, in the reference's idealised

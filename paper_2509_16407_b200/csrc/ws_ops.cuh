@@ -95,6 +95,24 @@ struct Ctx {
   __device__ __forceinline__ void unlock(u64 b) {
     if (!d.phased) unlock_bucket(d.locks, b);
   }
+  // Lock a bucket an insert routes INTO besides its primary.  Not part of the
+  // reference's discipline (openaddr.py:8-10 lets foreign writers rely on the
+  // slot CAS alone): with ~10^5 inserts in flight, unsynchronised
+  // least-loaded decisions read stale occupancy and overfill buckets, so a
+  // concurrent fill could report FULL where every sequential order succeeds.
+  // Holding the lock of every bucket whose occupancy drives a routing decision
+  // makes inserts serialisable.  Not counted as a probe (the reference's
+  // idealised accounting has no such lock).  Returns false when it had to
+  // drop `held` to respect ascending lock order -- the caller must re-read.
+  __device__ __forceinline__ bool lock_extra(u64 b, u64 held) {
+    if (d.phased) return true;
+    if (b > held) { lock_bucket(d.locks, b); return true; }
+    if (try_lock_bucket(d.locks, b)) return true;
+    unlock_bucket(d.locks, held);
+    lock_bucket(d.locks, b);
+    lock_bucket(d.locks, held);
+    return false;
+  }
   __device__ __forceinline__ void ldc(u64 i, u64& k, u64& v) { load_cell<RO>(cell(i), k, v); }
   __device__ __forceinline__ u16 ldt(u64 i) { return RO ? ld_tag_ro(d.tags + i) : ld_tag(d.tags + i); }
   __device__ __forceinline__ u64 hb(int i, u64 key, const Mod& m) const {
@@ -390,6 +408,8 @@ struct Ctx {
     const u16 tag = md_tag(h0);
     const bool locked = !d.lock_elided;
     u8 st;
+    bool have_b1 = false;
+    u64 b1_locked = 0;
     if (locked) lock(b0);
     for (;;) {
       Find r0 = find(b0, key, tag, false);
@@ -400,6 +420,11 @@ struct Ctx {
       if (!shortcut) {
         b1 = (i64)hb(1, key, d.nbm);
         if ((u64)b1 != b0) {
+          if (locked && !have_b1) {
+            have_b1 = true;
+            b1_locked = (u64)b1;
+            if (!lock_extra((u64)b1, b0)) continue;  // b0 was released: re-read it
+          }
           Find r1 = find((u64)b1, key, tag, false);
           if (r1.idx >= 0) { st = update(r1.idx, key, r1.val, val, merge); break; }
           used1 = r1.used;
@@ -425,6 +450,7 @@ struct Ctx {
       st = S_INSERTED;
       break;
     }
+    if (have_b1) unlock(b1_locked);
     if (locked) unlock(b0);
     return st;
   }
@@ -467,6 +493,9 @@ struct Ctx {
     const u64 b0 = d.frontm(h0 >> 16);
     const u16 tag = md_tag(h0);
     u8 st;
+    bool backs_locked = false;
+    u64 bl[2] = {0, 0};
+    int nbl = 0;
     lock(b0);
     for (;;) {
       Find r0 = find(b0, key, tag, false);
@@ -477,6 +506,13 @@ struct Ctx {
       if (!r0.saw_empty) {
         ice_backs(key, bk[0], bk[1]);
         nbk = bk[1] == bk[0] ? 1 : 2;
+        if (!backs_locked) {  // backyard indices exceed every front index: ascending order holds
+          backs_locked = true;
+          bl[0] = bk[0] < bk[1] ? bk[0] : bk[1];
+          bl[1] = bk[0] < bk[1] ? bk[1] : bk[0];
+          nbl = nbk;
+          for (int i = 0; i < nbl; i++) lock_extra(bl[i], b0);
+        }
         for (int i = 0; i < nbk; i++) {
           Find r = find(bk[i], key, tag, false);
           if (r.idx >= 0) { st = update(r.idx, key, r.val, val, merge); found = true; break; }
@@ -501,6 +537,7 @@ struct Ctx {
       st = S_INSERTED;
       break;
     }
+    for (int i = nbl - 1; i >= 0; i--) unlock(bl[i]);
     unlock(b0);
     return st;
   }
