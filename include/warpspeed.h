@@ -25,6 +25,7 @@
  *   ws_checksum               (new) size-independent content digest for parity at 2^28+
  *   ws_export_raw             slots.key_at / tags.get / arena words (test introspection)
  *   ws_info                   storage_report / arena.next_node / _tombstones_ever
+ *   ws_tune                   (new) performance knobs, no semantic effect
  *   ws_strerror               exception messages (InvalidKeyError / ConfigError)
  *
  * Semantics: a batch is a set of operations that execute concurrently on the
@@ -141,6 +142,11 @@ WS_API int ws_checksum(ws_table *t, uint64_t out[4], void *stream);
 WS_API int ws_export_raw(ws_table *t, uint64_t *words, uint64_t nwords, uint16_t *tags,
                   void *stream);
 WS_API int ws_info(ws_table *t, ws_info_t *info);
+
+/* performance knobs (no semantic effect) */
+#define WS_TUNE_QUERY_ILP 1 /* lookups in flight per thread in the tuned P2-MD query: 0 (generic kernel), 1, 2, 4, 8 */
+#define WS_TUNE_L2_POLICY 2 /* 1: tag loads L2 evict_last, cell loads evict_first */
+WS_API int ws_tune(ws_table *t, int knob, int value);
 
 WS_API const char *ws_strerror(int code);
 

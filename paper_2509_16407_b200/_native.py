@@ -28,7 +28,10 @@ WS_F_SERIAL = 4
 
 EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_erase", "ws_mixed",
            "ws_locate", "ws_probe_counts", "ws_occupied", "ws_export_items",
-           "ws_duplicate_scan", "ws_checksum", "ws_export_raw", "ws_info", "ws_strerror")
+           "ws_duplicate_scan", "ws_checksum", "ws_export_raw", "ws_info", "ws_tune",
+           "ws_strerror")
+WS_TUNE_QUERY_ILP = 1
+WS_TUNE_L2_POLICY = 2
 
 
 class WsConfig(C.Structure):
@@ -84,6 +87,7 @@ def load():
         lib.ws_checksum.argtypes = [vp, C.POINTER(u64 * 4), vp]
         lib.ws_export_raw.argtypes = [vp, vp, u64, vp, vp]
         lib.ws_info.argtypes = [vp, C.POINTER(WsInfo)]
+        lib.ws_tune.argtypes = [vp, i32, i32]
         lib.ws_strerror.argtypes = [i32]
         lib.ws_strerror.restype = C.c_char_p
         for name in EXPORTS:

@@ -420,6 +420,8 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.lock_elided = c.design == D_UNSAFE;
   d.line_bytes = c.line_bytes;
   d.wpn = 2 * c.bucket_size + 2;
+  d.tune_qilp = 4;
+  d.tune_l2pol = 0;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };
   if (c.design == D_CHAINING) {
@@ -703,6 +705,20 @@ int ws_export_raw(ws_table* t, uint64_t* words, uint64_t nwords, uint16_t* tags,
   }
   WS_CK(cudaStreamSynchronize(s));
   return WS_OK;
+}
+
+int ws_tune(ws_table* t, int knob, int value) {
+  if (!t) return WS_ERR_ARG;
+  switch (knob) {
+    case WS_TUNE_QUERY_ILP:
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return WS_ERR_ARG;
+      t->d.tune_qilp = value;
+      return WS_OK;
+    case WS_TUNE_L2_POLICY:
+      t->d.tune_l2pol = value ? 1 : 0;
+      return WS_OK;
+    default: return WS_ERR_ARG;
+  }
 }
 
 int ws_info(ws_table* t, ws_info_t* info) {

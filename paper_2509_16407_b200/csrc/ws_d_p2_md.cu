@@ -1,4 +1,44 @@
-// Kernel instantiations for the p2_md design (see ws_kernels.cuh).
+// Kernel instantiations for the p2_md design (the headline path): the generic
+// kernels of ws_kernels.cuh plus the tuned multi-lookup query of ws_fast.cuh.
+#include "ws_fast.cuh"
 #include "ws_kernels.cuh"
 
-WS_DEFINE_DESIGN(D_P2_MD, p2_md)
+namespace ws {
+
+template <int Q, bool RO, int POL>
+static void launch_fast_query(const QueryArgs& a) {
+  u64 g = (a.n + 256ull * Q - 1) / (256ull * Q);
+  if (g > (u64)kSMs * 8) g = (u64)kSMs * 8;
+  if (!g) g = 1;
+  k_query_p2md<Q, RO, POL><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase,
+                                                         a.gated);
+}
+
+template <int Q>
+static void fast_query_q(const QueryArgs& a) {
+  const bool pol = a.d.tune_l2pol != 0;
+  if (a.ro) { if (pol) launch_fast_query<Q, true, 1>(a); else launch_fast_query<Q, true, 0>(a); }
+  else { if (pol) launch_fast_query<Q, false, 1>(a); else launch_fast_query<Q, false, 0>(a); }
+}
+
+static void p2_md_ops(const OpsArgs& a, bool def) {
+  if (def) launch_ops_t<D_P2_MD, 32>(a); else launch_ops_t<D_P2_MD, 0>(a);
+}
+static void p2_md_query(const QueryArgs& a, bool def) {
+  if (!def || a.d.tune_qilp <= 0) {
+    if (def) launch_query_t<D_P2_MD, 32>(a); else launch_query_t<D_P2_MD, 0>(a);
+    return;
+  }
+  switch (a.d.tune_qilp) {
+    case 1: fast_query_q<1>(a); break;
+    case 2: fast_query_q<2>(a); break;
+    case 8: fast_query_q<8>(a); break;
+    default: fast_query_q<4>(a); break;
+  }
+}
+static void p2_md_locate(const LocateArgs& a, bool def) {
+  if (def) launch_locate_t<D_P2_MD, 32>(a); else launch_locate_t<D_P2_MD, 0>(a);
+}
+Launchers launchers_p2_md() { return Launchers{p2_md_ops, p2_md_query, p2_md_locate}; }
+
+}  // namespace ws

@@ -41,6 +41,8 @@ struct Dev {
   Mod nbm, frontm, backm;
   u64 seeds[8];
   int design, bs, md, shortcut, zcc, probe_cap, ways, depth, phased, lock_elided, line_bytes, wpn;
+  int tune_qilp;   // lookups per thread in the tuned query kernel (1, 2, 4)
+  int tune_l2pol;  // 1: tag loads evict_last, cell loads evict_first
 };
 
 __device__ __forceinline__ u64 apply_merge(int m, u64 old, u64 nv) {
@@ -282,9 +284,38 @@ struct Ctx {
   // reference openaddr.py:132-185: claim the first reusable slot of bucket b
   // (hint first) and publish (key, val); the md tag is written right after
   // the 128-bit publication.  Returns the slot or -1 when the bucket is full.
+  //
+  // Exclusive buckets: in P2 / iceberg / cuckoo every writer into a bucket's
+  // free slots holds that bucket's lock (see lock_extra), so a free slot seen
+  // under the lock cannot be taken concurrently and the 128-bit publication
+  // is a plain store -- no CAS, hence no DRAM read of the slot's sector.
+  static constexpr bool EXCL_DES = DES == D_P2 || DES == D_P2_MD || DES == D_ICEBERG ||
+                                   DES == D_ICEBERG_MD || DES == D_CUCKOO;
+  __device__ __forceinline__ bool exclusive() const { return EXCL_DES && !d.phased && !d.lock_elided; }
+
   __device__ i64 claim_publish(u64 b, i64 hint, u64 key, u64 val, u16 tag) {
     const int n = B();
     const u64 lo = b * (u64)n, hi = lo + n;
+    if (exclusive()) {
+      if constexpr (!MD) {
+        if (hint < 0) hint = find_free(lo, n);
+        if (hint < 0) return -1;
+        st_cell(cell((u64)hint), key, val);
+        touch(16 * (u64)hint);
+        return hint;
+      } else {
+        const i64 z = hint >= 0 ? hint : md_first_zero(lo, hi, lo);
+        if (z < 0) return -1;
+        touch(16 * (u64)z);
+        // a zero tag may be a slot an eraser just tombstoned: order its
+        // tombstone store (released by the eraser's fence) before ours
+        if (conc_erase) fence_acq_rel();
+        st_cell(cell((u64)z), key, val);
+        st_tag(d.tags + z, tag);
+        touch(TAG_BASE + 2 * (u64)z);
+        return z;
+      }
+    }
     if constexpr (!MD) {
       for (;;) {
         if (hint < 0) hint = find_free(lo, n);
@@ -329,6 +360,7 @@ struct Ctx {
     st_cell(cell(idx), TOMB, 0);
     touch(16 * idx);
     if constexpr (MD) {
+      fence_acq_rel();  // the tombstone is visible before the zero tag that advertises it
       st_tag(d.tags + idx, 0);
       touch(TAG_BASE + 2 * idx);
     }
@@ -410,6 +442,8 @@ struct Ctx {
     u8 st;
     bool have_b1 = false;
     u64 b1_locked = 0;
+    // start the primary tag block's DRAM fetch while the lock round trip runs
+    if constexpr (MD) asm volatile("prefetch.global.L2 [%0];" :: "l"(d.tags + b0 * 32));
     if (locked) lock(b0);
     for (;;) {
       Find r0 = find(b0, key, tag, false);

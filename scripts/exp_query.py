@@ -1,0 +1,51 @@
+"""Experiment: tuned P2-MD query variants (lookups/thread x L2 policy) and insert time."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2509_16407_b200 import TableConfig, make_table
+from paper_2509_16407_b200.workload import derive_seed, gen_uniform_keys
+
+lg = int(sys.argv[1]) if len(sys.argv) > 1 else 28
+slots = 1 << lg
+n = int(slots * 0.9)
+t = make_table(TableConfig(design="p2_md", capacity_slots=slots, seed=42))
+keys = torch.from_numpy(gen_uniform_keys(42, n).view(np.int64)).cuda()
+vals = keys & 0xFFFF
+miss = torch.from_numpy(gen_uniform_keys(derive_seed(42, 0xFEED), n - n // 2).view(np.int64)).cuda()
+q = torch.cat([keys[: n // 2], miss])
+q = q[torch.randperm(n, device="cuda")].view(torch.uint64)
+
+
+def timed(fn, reps=3):
+    best = 1e9
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        r = fn()
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b))
+    return best, r
+
+
+ins = []
+for rep in range(3):
+    t.clear()
+    ms, st = timed(lambda: t.upsert_batch(keys.view(torch.uint64), vals.view(torch.uint64), check=False), 1)
+    ins.append(ms)
+    assert int((st != 0).sum()) == 0
+print(f"insert {min(ins):.2f} ms  ({n / min(ins) / 1e6:.2f} G/s)", flush=True)
+ref_f, ref_v = None, None
+for ilp in (0, 1, 2, 4, 8):
+    for pol in (0, 1):
+        t.tune(query_ilp=ilp, l2_policy=pol)
+        ms, (f, v) = timed(lambda: t.query_batch(q, check=False))
+        if ref_f is None:
+            ref_f, ref_v = f.clone(), v.clone()
+        ok = torch.equal(f, ref_f) and torch.equal(v.view(torch.int64), ref_v.view(torch.int64))
+        print(f"query ilp={ilp} pol={pol}: {ms:.2f} ms ({n / ms / 1e6:.2f} G/s) same={ok} hits={int(f.sum())}",
+              flush=True)

@@ -1,0 +1,107 @@
+// gather_bench.cu -- B200 random-access ceilings for the hash-table roofline.
+//
+// Each thread performs R independent random reads of W bytes (W = 16, 32, 64,
+// 128) at W-aligned positions of a large buffer (>> L2), addresses from a
+// splitmix64 hash (no index array), and XOR-folds the data.  Variants:
+//   flavor 0: weak loads (ld.global, L1 allocate)
+//   flavor 1: ld.global.nc.L1::no_allocate
+//   flavor 2: ld.relaxed.gpu (coherent, what mutating kernels use)
+//   flavor 3: ld.global.L2::64B hint (nc)
+// Prints useful GB/s and G accesses/s; run under ncu for DRAM sectors/access.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_bench gather_bench.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 mix64(u64 x) {
+  x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+  return x;
+}
+
+template <int FL>
+__device__ __forceinline__ void ld16(const void* p, u64& a, u64& b) {
+  if (FL == 0) asm volatile("ld.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  else if (FL == 1) asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  else if (FL == 2) asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+  else asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
+template <int FL>
+__device__ __forceinline__ void ld32(const void* p, u64& a, u64& b, u64& c, u64& d) {
+  if (FL == 0) asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+  else if (FL == 1) asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+  else if (FL == 2) asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+  else asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(a), "=l"(b), "=l"(c), "=l"(d) : "l"(p));
+}
+
+template <int W, int FL, int R>
+__global__ void __launch_bounds__(256) gather(const char* buf, u64 nunits, u64 seed, u64* out, int iters) {
+  u64 acc = 0;
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; it++) {
+    u64 idx[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) idx[r] = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) % nunits;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const char* p = buf + idx[r] * W;
+      if (W == 16) { u64 a, b; ld16<FL>(p, a, b); acc ^= a ^ b; }
+      else {
+#pragma unroll
+        for (int o = 0; o < W; o += 32) { u64 a, b, c, d; ld32<FL>(p + o, a, b, c, d); acc ^= a ^ b ^ c ^ d; }
+      }
+    }
+  }
+  if (acc == 0x123456789ull) out[0] = acc;
+}
+
+template <int W, int FL, int R>
+void run(const char* buf, u64 bytes, u64* out, int blocks, int iters, const char* name) {
+  const u64 nunits = bytes / W;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  gather<W, FL, R><<<blocks, 256>>>(buf, nunits, 1, out, 1);
+  cudaEventRecord(a);
+  gather<W, FL, R><<<blocks, 256>>>(buf, nunits, 7, out, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double acc = (double)blocks * 256 * R * iters;
+  printf("%-28s W=%4d R=%d  %8.2f G acc/s  %8.1f GB/s useful\n", name, W, R, acc / ms / 1e6, acc * W / ms / 1e6);
+}
+
+int main(int argc, char** argv) {
+  const u64 mb = argc > 1 ? strtoull(argv[1], 0, 10) : 4096;
+  const u64 bytes = mb << 20;
+  printf("buffer %llu MiB\n", mb);
+  char* buf; u64* out;
+  cudaMalloc(&buf, bytes); cudaMalloc(&out, 64);
+  cudaMemset(buf, 1, bytes);
+  const int blocks = 148 * 8, iters = 16;
+  if (argc > 2) {  // short sweep
+    run<32, 1, 8>(buf, bytes, out, blocks, iters, "nc 32B");
+    run<32, 3, 8>(buf, bytes, out, blocks, iters, "nc L2::64B 32B");
+    run<16, 1, 8>(buf, bytes, out, blocks, iters, "nc 16B");
+    cudaDeviceSynchronize();
+    return 0;
+  }
+  run<16, 0, 8>(buf, bytes, out, blocks, iters, "weak 16B");
+  run<16, 1, 8>(buf, bytes, out, blocks, iters, "nc 16B");
+  run<16, 2, 8>(buf, bytes, out, blocks, iters, "relaxed 16B");
+  run<16, 3, 8>(buf, bytes, out, blocks, iters, "nc L2::64B 16B");
+  run<32, 0, 8>(buf, bytes, out, blocks, iters, "weak 32B");
+  run<32, 1, 8>(buf, bytes, out, blocks, iters, "nc 32B");
+  run<32, 2, 8>(buf, bytes, out, blocks, iters, "relaxed 32B");
+  run<32, 3, 8>(buf, bytes, out, blocks, iters, "nc L2::64B 32B");
+  run<64, 1, 8>(buf, bytes, out, blocks, iters, "nc 64B");
+  run<64, 2, 8>(buf, bytes, out, blocks, iters, "relaxed 64B");
+  run<128, 1, 4>(buf, bytes, out, blocks, iters, "nc 128B");
+  run<128, 2, 4>(buf, bytes, out, blocks, iters, "relaxed 128B");
+  run<16, 1, 2>(buf, bytes, out, blocks, iters, "nc 16B low-MLP");
+  run<16, 1, 16>(buf, bytes, out, blocks, iters, "nc 16B high-MLP");
+  cudaError_t e = cudaDeviceSynchronize();
+  printf("%s\n", cudaGetErrorString(e));
+  return 0;
+}
