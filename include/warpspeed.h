@@ -144,7 +144,8 @@ WS_API int ws_export_raw(ws_table *t, uint64_t *words, uint64_t nwords, uint16_t
 WS_API int ws_info(ws_table *t, ws_info_t *info);
 
 /* performance knobs (no semantic effect) */
-#define WS_TUNE_QUERY_ILP 1 /* lookups in flight per thread in the tuned P2-MD query: 0 (generic kernel), 1, 2, 4, 8 */
+#define WS_TUNE_QUERY_ILP 1 /* P2-MD kernel variant: 3 = lane-pair tiles (default), 1/2/4/8 = lookups
+                               per thread, 0 = generic kernels, -1 = generic kernels for upserts too */
 #define WS_TUNE_L2_POLICY 2 /* 1: tag loads L2 evict_last, cell loads evict_first */
 WS_API int ws_tune(ws_table *t, int knob, int value);
 

@@ -420,7 +420,7 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.lock_elided = c.design == D_UNSAFE;
   d.line_bytes = c.line_bytes;
   d.wpn = 2 * c.bucket_size + 2;
-  d.tune_qilp = 4;
+  d.tune_qilp = 3;
   d.tune_l2pol = 0;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };
@@ -711,7 +711,7 @@ int ws_tune(ws_table* t, int knob, int value) {
   if (!t) return WS_ERR_ARG;
   switch (knob) {
     case WS_TUNE_QUERY_ILP:
-      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8) return WS_ERR_ARG;
+      if (value < -1 || value > 8) return WS_ERR_ARG;
       t->d.tune_qilp = value;
       return WS_OK;
     case WS_TUNE_L2_POLICY:

@@ -3,6 +3,8 @@
 #include "ws_fast.cuh"
 #include "ws_kernels.cuh"
 
+#include <algorithm>
+
 namespace ws {
 
 template <int Q, bool RO, int POL>
@@ -22,6 +24,17 @@ static void fast_query_q(const QueryArgs& a) {
 }
 
 static void p2_md_ops(const OpsArgs& a, bool def) {
+  // lane-pair upsert: uniform-upsert launches on exclusive (locked) tables
+  const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
+  if (def && upsert_only && !a.instr && !a.serial && !a.redo && !a.d.phased && !a.d.lock_elided &&
+      a.d.tune_qilp >= 0) {
+    u64 g = (2 * a.n + 255) / 256;
+    const u64 lim = std::max<u64>((2 * a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
+    g = std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim);
+    k_upsert_p2md_pair<<<(unsigned)std::max<u64>(g, 1), 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4,
+                                                                       a.status, a.conc_erase, a.gated);
+    return;
+  }
   if (def) launch_ops_t<D_P2_MD, 32>(a); else launch_ops_t<D_P2_MD, 0>(a);
 }
 static void p2_md_query(const QueryArgs& a, bool def) {
@@ -30,6 +43,13 @@ static void p2_md_query(const QueryArgs& a, bool def) {
     return;
   }
   switch (a.d.tune_qilp) {
+    case 3: {  // lane-pair tile (one line request per tag block)
+      u64 g = (2 * a.n + 255) / 256;
+      g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * 8);
+      if (a.ro) k_query_p2md_pair<true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated);
+      else k_query_p2md_pair<false><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated);
+      break;
+    }
     case 1: fast_query_q<1>(a); break;
     case 2: fast_query_q<2>(a); break;
     case 8: fast_query_q<8>(a); break;

@@ -156,4 +156,196 @@ __global__ void __launch_bounds__(256) k_query_p2md(Dev d, const u64* __restrict
   }
 }
 
+// ===================================================== lane-pair kernels
+//
+// A 2-lane cooperative tile owns one operation.  Each lane loads one 32-byte
+// half of the 64-byte tag block, so the warp instruction carries ONE line
+// request per operation instead of two (beyond L2 the B200 sustains ~45 G
+// L2-missing requests/s, scripts/gather_bench.cu; a single thread reading 64 B
+// issues 2).  The lanes exchange their 16-slot masks with one shuffle and then
+// run identical control flow on identical data; loads of the same address by
+// both lanes in one instruction merge into one request.  Side effects (lock
+// atomics, publication stores) are issued by the even lane only.
+
+struct Pair {
+  u32 mask;
+  int half;
+  __device__ __forceinline__ Pair() {
+    const int lane = threadIdx.x & 31;
+    half = lane & 1;
+    mask = 3u << (lane & 30);
+  }
+  __device__ __forceinline__ u32 xchg(u32 v) const { return __shfl_xor_sync(mask, v, 1); }
+  __device__ __forceinline__ u32 from_lead(u32 v) const { return __shfl_sync(mask, v, (threadIdx.x & 31) & 30); }
+};
+
+template <bool RO>
+__device__ __forceinline__ void pair_masks(const Dev& d, const Pair& p, u64 b, u16 tag, u32& M, u32& Z) {
+  u32 w[8];
+  const u16* blk = d.tags + b * 32 + p.half * 16;
+  if (RO) ld_tags32_ro(blk, w); else ld_tags32(blk, w);
+  const u32 pat = (u32)tag * 0x10001u;
+  u32 m = 0, z = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const u32 mm = __vcmpeq2(w[i], pat), zz = __vcmpeq2(w[i], 0u);
+    m |= ((mm & 1u) | ((mm >> 15) & 2u)) << (2 * i);
+    z |= ((zz & 1u) | ((zz >> 15) & 2u)) << (2 * i);
+  }
+  const u32 om = p.xchg(m), oz = p.xchg(z);
+  M = p.half ? (om | (m << 16)) : (m | (om << 16));
+  Z = p.half ? (oz | (z << 16)) : (z | (oz << 16));
+}
+
+// first slot (0..31) of bucket b holding key among the tag matches M, or -1
+template <bool RO>
+__device__ __forceinline__ int pair_confirm(const Dev& d, u64 b, u32 M, u64 key, u64& val) {
+  while (M) {
+    const int j = __ffs(M) - 1;
+    M &= M - 1;
+    u64 k, v;
+    load_cell<RO>(d.cells + 2 * (b * 32 + j), k, v);
+    if (k == key) { val = v; return j; }
+  }
+  return -1;
+}
+
+template <bool RO>
+__global__ void __launch_bounds__(256) k_query_p2md_pair(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
+                                                         u8* found, int conc_erase, int gated) {
+  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  const Pair p;
+  const u32 te0 = ld_u32_relaxed(d.state);
+  const u64 stride = ((u64)gridDim.x * blockDim.x) >> 1;
+  for (u64 i = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 1; i < n; i += stride) {
+    const u64 key = __ldg(keys + i);
+    const u64 h0 = mix64(key ^ d.seeds[0]);
+    const u64 b0 = d.nbm(h0 >> 16);
+    const u16 t = (u16)(h0 & 0xFFFF);
+    const u16 tag = t ? t : (u16)1;
+    u32 M, Z;
+    pair_masks<RO>(d, p, b0, tag, M, Z);
+    u64 val = 0;
+    bool hit = M && pair_confirm<RO>(d, b0, M, key, val) >= 0;
+    if (!hit) {
+      bool te = te0 != 0;
+      if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
+      const int zc = __popc(Z);
+      const int used0 = 32 - (zc < d.zcc ? zc : d.zcc);
+      if (!(Z && !te && used0 < d.shortcut)) {  // no early exit (openaddr.py:440-442)
+        const u64 b1 = d.nbm(mix64(key ^ d.seeds[1]) >> 16);
+        if (b1 != b0) {
+          pair_masks<RO>(d, p, b1, tag, M, Z);
+          hit = M && pair_confirm<RO>(d, b1, M, key, val) >= 0;
+        }
+      }
+    }
+    if (p.half == 0) {
+      if (found) found[i] = hit;
+      if (vout) vout[i] = hit ? val : 0;
+    }
+  }
+}
+
+// P2-MD upsert (reference openaddr.py:370-418 plus the serialisable routing
+// of Ctx::p2_upsert) for exclusive-mode tables (locks on, not lock-elided).
+__device__ __forceinline__ void pair_lock(const Dev& d, const Pair& p, u64 b) {
+  if (p.half == 0) lock_bucket(d.locks, b);
+  __syncwarp(p.mask);
+}
+__device__ __forceinline__ void pair_unlock(const Dev& d, const Pair& p, u64 b) {
+  __syncwarp(p.mask);
+  if (p.half == 0) unlock_bucket(d.locks, b);
+}
+// extra bucket lock in ascending order; false when `held` had to be dropped
+__device__ __forceinline__ bool pair_lock_extra(const Dev& d, const Pair& p, u64 b, u64 held) {
+  u32 ok = 1;
+  if (p.half == 0) {
+    if (b > held) {
+      lock_bucket(d.locks, b);
+    } else if (!try_lock_bucket(d.locks, b)) {
+      unlock_bucket(d.locks, held);
+      lock_bucket(d.locks, b);
+      lock_bucket(d.locks, held);
+      ok = 0;
+    }
+  }
+  return p.from_lead(ok) != 0;
+}
+
+__global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __restrict__ keys,
+                                                          const u64* __restrict__ vals, u64 n, int merge,
+                                                          u8* status, int conc_erase, int gated) {
+  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  const Pair p;
+  const bool lead = p.half == 0;
+  const u32 te0 = ld_u32_relaxed(d.state);
+  const u64 stride = ((u64)gridDim.x * blockDim.x) >> 1;
+  for (u64 i = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 1; i < n; i += stride) {
+    const u64 key = __ldg(keys + i);
+    const u64 val = __ldg(vals + i);
+    const u64 h0 = mix64(key ^ d.seeds[0]);
+    const u64 b0 = d.nbm(h0 >> 16);
+    const u16 t = (u16)(h0 & 0xFFFF);
+    const u16 tag = t ? t : (u16)1;
+    bool have_b1 = false;
+    u64 b1l = 0;
+    u8 st;
+    pair_lock(d, p, b0);
+    for (;;) {
+      u32 M0, Z0;
+      pair_masks<false>(d, p, b0, tag, M0, Z0);
+      u64 old;
+      int j = M0 ? pair_confirm<false>(d, b0, M0, key, old) : -1;
+      if (j >= 0) {
+        if (lead) st_cell(d.cells + 2 * (b0 * 32 + j), key, apply_merge(merge, old, val));
+        st = S_UPDATED;
+        break;
+      }
+      bool te = te0 != 0;
+      if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
+      const int zc0 = __popc(Z0);
+      const int used0 = 32 - (zc0 < d.zcc ? zc0 : d.zcc);
+      u64 target = b0;
+      u32 Zt = Z0;
+      if (te || used0 >= d.shortcut) {  // no shortcut: consult the alternate
+        const u64 b1 = d.nbm(mix64(key ^ d.seeds[1]) >> 16);
+        if (b1 != b0) {
+          if (!have_b1) {
+            have_b1 = true;
+            b1l = b1;
+            if (!pair_lock_extra(d, p, b1, b0)) continue;  // b0 was dropped: re-read it
+          }
+          u32 M1, Z1;
+          pair_masks<false>(d, p, b1, tag, M1, Z1);
+          j = M1 ? pair_confirm<false>(d, b1, M1, key, old) : -1;
+          if (j >= 0) {
+            if (lead) st_cell(d.cells + 2 * (b1 * 32 + j), key, apply_merge(merge, old, val));
+            st = S_UPDATED;
+            break;
+          }
+          const int zc1 = __popc(Z1);
+          const int used1 = 32 - (zc1 < d.zcc ? zc1 : d.zcc);
+          const bool prim = used0 <= used1;  // ties go to the primary
+          target = prim ? b0 : b1;
+          Zt = prim ? Z0 : Z1;
+          if (!Zt) { target = prim ? b1 : b0; Zt = prim ? Z1 : Z0; }
+        }
+      }
+      if (!Zt) { st = S_FULL; break; }
+      const u64 slot = target * 32 + (__ffs(Zt) - 1);
+      if (lead) {
+        if (conc_erase) fence_acq_rel();
+        st_cell(d.cells + 2 * slot, key, val);
+        st_tag(d.tags + slot, tag);
+      }
+      st = S_INSERTED;
+      break;
+    }
+    if (have_b1) pair_unlock(d, p, b1l);
+    pair_unlock(d, p, b0);
+    if (lead && status) status[i] = st;
+  }
+}
+
 }  // namespace ws

@@ -442,8 +442,6 @@ struct Ctx {
     u8 st;
     bool have_b1 = false;
     u64 b1_locked = 0;
-    // start the primary tag block's DRAM fetch while the lock round trip runs
-    if constexpr (MD) asm volatile("prefetch.global.L2 [%0];" :: "l"(d.tags + b0 * 32));
     if (locked) lock(b0);
     for (;;) {
       Find r0 = find(b0, key, tag, false);
