@@ -422,6 +422,7 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.wpn = 2 * c.bucket_size + 2;
   d.tune_qilp = 3;
   d.tune_l2pol = 0;
+  d.tune_upsert = 0;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };
   if (c.design == D_CHAINING) {
@@ -716,6 +717,10 @@ int ws_tune(ws_table* t, int knob, int value) {
       return WS_OK;
     case WS_TUNE_L2_POLICY:
       t->d.tune_l2pol = value ? 1 : 0;
+      return WS_OK;
+    case WS_TUNE_UPSERT:
+      if (value < 0 || value > 1) return WS_ERR_ARG;
+      t->d.tune_upsert = value;
       return WS_OK;
     default: return WS_ERR_ARG;
   }

@@ -27,7 +27,7 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
   // lane-pair upsert: uniform-upsert launches on exclusive (locked) tables
   const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
   if (def && upsert_only && !a.instr && !a.serial && !a.redo && !a.d.phased && !a.d.lock_elided &&
-      a.d.tune_qilp >= 0) {
+      a.d.tune_upsert == 1) {
     u64 g = (2 * a.n + 255) / 256;
     const u64 lim = std::max<u64>((2 * a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
     g = std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim);

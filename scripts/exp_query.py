@@ -32,15 +32,19 @@ def timed(fn, reps=3):
     return best, r
 
 
-ins = []
-for rep in range(3):
-    t.clear()
-    ms, st = timed(lambda: t.upsert_batch(keys.view(torch.uint64), vals.view(torch.uint64), check=False), 1)
-    ins.append(ms)
-    assert int((st != 0).sum()) == 0
-print(f"insert {min(ins):.2f} ms  ({n / min(ins) / 1e6:.2f} G/s)", flush=True)
+for variant in (-1, 3):
+    t.tune(query_ilp=variant)
+    ins = []
+    for rep in range(3):
+        t.clear()
+        ms, st = timed(lambda: t.upsert_batch(keys.view(torch.uint64), vals.view(torch.uint64), check=False), 1)
+        ins.append(ms)
+        bad = int((st != 0).sum())
+    cs = t.checksum()
+    print(f"insert variant {variant}: {min(ins):.2f} ms  ({n / min(ins) / 1e6:.2f} G/s) bad={bad} occupied={cs[0]}",
+          flush=True)
 ref_f, ref_v = None, None
-for ilp in (0, 1, 2, 4, 8):
+for ilp in (0, 3, 1, 4):
     for pol in (0, 1):
         t.tune(query_ilp=ilp, l2_policy=pol)
         ms, (f, v) = timed(lambda: t.query_batch(q, check=False))
