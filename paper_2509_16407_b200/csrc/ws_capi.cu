@@ -716,10 +716,11 @@ int ws_tune(ws_table* t, int knob, int value) {
       t->d.tune_qilp = value;
       return WS_OK;
     case WS_TUNE_L2_POLICY:
-      t->d.tune_l2pol = value ? 1 : 0;
+      if (value < 0 || value > 2) return WS_ERR_ARG;
+      t->d.tune_l2pol = value;
       return WS_OK;
     case WS_TUNE_UPSERT:
-      if (value < 0 || value > 1) return WS_ERR_ARG;
+      if (value < 0 || value > 3) return WS_ERR_ARG;
       t->d.tune_upsert = value;
       return WS_OK;
     default: return WS_ERR_ARG;

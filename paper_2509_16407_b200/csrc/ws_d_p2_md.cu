@@ -18,7 +18,7 @@ static void launch_fast_query(const QueryArgs& a) {
 
 template <int Q>
 static void fast_query_q(const QueryArgs& a) {
-  const bool pol = a.d.tune_l2pol != 0;
+  const bool pol = a.d.tune_l2pol == 1;
   if (a.ro) { if (pol) launch_fast_query<Q, true, 1>(a); else launch_fast_query<Q, true, 0>(a); }
   else { if (pol) launch_fast_query<Q, false, 1>(a); else launch_fast_query<Q, false, 0>(a); }
 }
@@ -35,6 +35,19 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
                                                                        a.status, a.conc_erase, a.gated);
     return;
   }
+  if (def && upsert_only && !a.instr && !a.serial && !a.redo && !a.d.phased && !a.d.lock_elided &&
+      a.d.tune_upsert >= 2) {
+    u64 g = (a.n + 255) / 256;
+    const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
+    if (a.d.tune_upsert == 3)
+      k_upsert_p2md_rounds<true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status,
+                                                               a.conc_erase, a.gated);
+    else
+      k_upsert_p2md_rounds<false><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status,
+                                                                a.conc_erase, a.gated);
+    return;
+  }
   if (def) launch_ops_t<D_P2_MD, 32>(a); else launch_ops_t<D_P2_MD, 0>(a);
 }
 static void p2_md_query(const QueryArgs& a, bool def) {
@@ -46,8 +59,11 @@ static void p2_md_query(const QueryArgs& a, bool def) {
     case 3: {  // lane-pair tile (one line request per tag block)
       u64 g = (2 * a.n + 255) / 256;
       g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * 8);
-      if (a.ro) k_query_p2md_pair<true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated);
-      else k_query_p2md_pair<false><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated);
+#define WS_QP(RO, F) k_query_p2md_pair<RO, F><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated)
+      const bool f64 = a.d.tune_l2pol == 2;
+      if (a.ro) { if (f64) WS_QP(true, true); else WS_QP(true, false); }
+      else { if (f64) WS_QP(false, true); else WS_QP(false, false); }
+#undef WS_QP
       break;
     }
     case 1: fast_query_q<1>(a); break;

@@ -179,11 +179,35 @@ struct Pair {
   __device__ __forceinline__ u32 from_lead(u32 v) const { return __shfl_sync(mask, v, (threadIdx.x & 31) & 30); }
 };
 
-template <bool RO>
+// 64-byte L2 fetch: the default promotes every random miss to a 128-byte
+// line fill (4 sectors, measured); a 64-byte tag block or a 16-byte cell only
+// needs 2 (scripts/gather_bench.cu: 3.92 -> 1.98 DRAM sectors per access).
+__device__ __forceinline__ void ld_tags32_64(const u16* p, u32 (&w)[8]) {
+  asm volatile("ld.relaxed.gpu.global.L2::64B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ld_tags32_ro64(const u16* p, u32 (&w)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
+template <bool RO, bool F64>
+__device__ __forceinline__ void ld_cell_f(const u64* p, u64& k, u64& v) {
+  if (!F64) { load_cell<RO>(p, k, v); return; }
+  if (RO)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v2.u64 {%0, %1}, [%2];" : "=l"(k), "=l"(v) : "l"(p));
+  else
+    asm volatile("{.reg .b128 t; ld.relaxed.gpu.global.L2::64B.b128 t, [%2]; mov.b128 {%0, %1}, t;}"
+                 : "=l"(k), "=l"(v) : "l"(p) : "memory");
+}
+
+template <bool RO, bool F64 = false>
 __device__ __forceinline__ void pair_masks(const Dev& d, const Pair& p, u64 b, u16 tag, u32& M, u32& Z) {
   u32 w[8];
   const u16* blk = d.tags + b * 32 + p.half * 16;
-  if (RO) ld_tags32_ro(blk, w); else ld_tags32(blk, w);
+  if (F64) { if (RO) ld_tags32_ro64(blk, w); else ld_tags32_64(blk, w); }
+  else { if (RO) ld_tags32_ro(blk, w); else ld_tags32(blk, w); }
   const u32 pat = (u32)tag * 0x10001u;
   u32 m = 0, z = 0;
 #pragma unroll
@@ -198,19 +222,19 @@ __device__ __forceinline__ void pair_masks(const Dev& d, const Pair& p, u64 b, u
 }
 
 // first slot (0..31) of bucket b holding key among the tag matches M, or -1
-template <bool RO>
+template <bool RO, bool F64 = false>
 __device__ __forceinline__ int pair_confirm(const Dev& d, u64 b, u32 M, u64 key, u64& val) {
   while (M) {
     const int j = __ffs(M) - 1;
     M &= M - 1;
     u64 k, v;
-    load_cell<RO>(d.cells + 2 * (b * 32 + j), k, v);
+    ld_cell_f<RO, F64>(d.cells + 2 * (b * 32 + j), k, v);
     if (k == key) { val = v; return j; }
   }
   return -1;
 }
 
-template <bool RO>
+template <bool RO, bool F64>
 __global__ void __launch_bounds__(256) k_query_p2md_pair(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                          u8* found, int conc_erase, int gated) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
@@ -224,9 +248,9 @@ __global__ void __launch_bounds__(256) k_query_p2md_pair(Dev d, const u64* __res
     const u16 t = (u16)(h0 & 0xFFFF);
     const u16 tag = t ? t : (u16)1;
     u32 M, Z;
-    pair_masks<RO>(d, p, b0, tag, M, Z);
+    pair_masks<RO, F64>(d, p, b0, tag, M, Z);
     u64 val = 0;
-    bool hit = M && pair_confirm<RO>(d, b0, M, key, val) >= 0;
+    bool hit = M && pair_confirm<RO, F64>(d, b0, M, key, val) >= 0;
     if (!hit) {
       bool te = te0 != 0;
       if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
@@ -235,8 +259,8 @@ __global__ void __launch_bounds__(256) k_query_p2md_pair(Dev d, const u64* __res
       if (!(Z && !te && used0 < d.shortcut)) {  // no early exit (openaddr.py:440-442)
         const u64 b1 = d.nbm(mix64(key ^ d.seeds[1]) >> 16);
         if (b1 != b0) {
-          pair_masks<RO>(d, p, b1, tag, M, Z);
-          hit = M && pair_confirm<RO>(d, b1, M, key, val) >= 0;
+          pair_masks<RO, F64>(d, p, b1, tag, M, Z);
+          hit = M && pair_confirm<RO, F64>(d, b1, M, key, val) >= 0;
         }
       }
     }
@@ -345,6 +369,136 @@ __global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __re
     if (have_b1) pair_unlock(d, p, b1l);
     pair_unlock(d, p, b0);
     if (lead && status) status[i] = st;
+  }
+}
+
+// =============================================== warp-synchronous rounds
+//
+// P2-MD upsert, one thread per op, in warp-synchronous lock rounds.  A
+// release fence (MEMBAR.GPU) waits for every memory operation the warp has in
+// flight; issued per lane at unlock time -- while warp-mates still have DRAM
+// loads outstanding -- it was 35% of the one-thread kernel's stall samples.
+// Here each round is:
+//   1. every pending lane TRY-locks its primary (atom.acquire; never blocks),
+//   2. lanes holding their lock read tags, decide, try-lock the alternate if
+//      routing needs it (serialisable routing, see Ctx::lock_extra) and
+//      publish (plain 128-bit store + tag store, exclusive bucket),
+//   3. the warp reconverges and issues ONE fence.acq_rel, then every lane
+//      releases its locks with relaxed reds (fence-based release),
+//   4. lanes whose try-lock failed keep their op for the next round (after a
+//      lane-staggered backoff, holding no lock -- no deadlock, and warp-mates
+//      never wait on each other's locks).
+template <bool F64>
+__device__ __forceinline__ void tag_masks_t(const Dev& d, u64 b, u16 tag, u32& M, u32& Z) {
+  u32 a[8], c[8];
+  const u16* blk = d.tags + b * 32;
+  if (F64) { ld_tags32_64(blk, a); ld_tags32_64(blk + 16, c); }
+  else { ld_tags32(blk, a); ld_tags32(blk + 16, c); }
+  masks_from(a, c, tag, M, Z);
+}
+
+__device__ __forceinline__ u32 atom_or_relaxed(u32* p, u32 m) {
+  u32 old;
+  asm volatile("atom.relaxed.gpu.global.or.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(m) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_and_relaxed(u32* p, u32 m) {
+  asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" :: "l"(p), "r"(m) : "memory");
+}
+
+template <bool F64>
+__global__ void __launch_bounds__(256) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
+                                                            const u64* __restrict__ vals, u64 n, int merge,
+                                                            u8* status, int conc_erase, int gated) {
+  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  const u32 te0 = ld_u32_relaxed(d.state);
+  const int lane = threadIdx.x & 31;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c * 32 < n; c += nwarps) {
+    const u64 i = c * 32 + lane;
+    bool pending = i < n;
+    u64 key = 0, val = 0, b0 = 0, b1 = 0;
+    u16 tag = 1;
+    if (pending) {
+      key = __ldg(keys + i);
+      val = __ldg(vals + i);
+      const u64 h0 = mix64(key ^ d.seeds[0]);
+      b0 = d.nbm(h0 >> 16);
+      const u16 t = (u16)(h0 & 0xFFFF);
+      tag = t ? t : (u16)1;
+      b1 = d.nbm(mix64(key ^ d.seeds[1]) >> 16);
+    }
+    u8 st = 0;
+    unsigned backoff = 64;
+    while (__any_sync(0xFFFFFFFFu, pending)) {
+      bool hold0 = false, hold1 = false;
+      if (pending) {
+        hold0 = try_lock_bucket(d.locks, b0);
+        if (hold0) {
+          u32 M0, Z0;
+          tag_masks_t<F64>(d, b0, tag, M0, Z0);
+          u64 old;
+          int j = M0 ? pair_confirm<false, F64>(d, b0, M0, key, old) : -1;
+          if (j >= 0) {
+            st_cell(d.cells + 2 * (b0 * 32 + j), key, apply_merge(merge, old, val));
+            st = S_UPDATED;
+            pending = false;
+          } else {
+            bool te = te0 != 0;
+            if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
+            const int zc0 = __popc(Z0);
+            const int used0 = 32 - (zc0 < d.zcc ? zc0 : d.zcc);
+            u64 target = b0;
+            u32 Zt = Z0;
+            bool decided = true;
+            if ((te || used0 >= d.shortcut) && b1 != b0) {
+              hold1 = try_lock_bucket(d.locks, b1);
+              if (!hold1) {
+                decided = false;  // retry the whole op next round
+              } else {
+                u32 M1, Z1;
+                tag_masks_t<F64>(d, b1, tag, M1, Z1);
+                j = M1 ? pair_confirm<false, F64>(d, b1, M1, key, old) : -1;
+                if (j >= 0) {
+                  st_cell(d.cells + 2 * (b1 * 32 + j), key, apply_merge(merge, old, val));
+                  st = S_UPDATED;
+                  pending = false;
+                  decided = false;
+                } else {
+                  const int zc1 = __popc(Z1);
+                  const int used1 = 32 - (zc1 < d.zcc ? zc1 : d.zcc);
+                  const bool prim = used0 <= used1;  // ties go to the primary
+                  target = prim ? b0 : b1;
+                  Zt = prim ? Z0 : Z1;
+                  if (!Zt) { target = prim ? b1 : b0; Zt = prim ? Z1 : Z0; }
+                }
+              }
+            }
+            if (decided) {
+              if (!Zt) {
+                st = S_FULL;
+              } else {
+                const u64 slot = target * 32 + (__ffs(Zt) - 1);
+                if (conc_erase) fence_acq_rel();
+                st_cell(d.cells + 2 * slot, key, val);
+                st_tag(d.tags + slot, tag);
+                st = S_INSERTED;
+              }
+              pending = false;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      fence_acq_rel();  // one MEMBAR per warp-round: publications before the unlocks
+      if (hold1) red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
+      if (hold0) red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+      if (pending) {
+        __nanosleep(backoff + 8 * lane);
+        if (backoff < 4096) backoff <<= 1;
+      }
+    }
+    if (i < n && status) status[i] = st;
   }
 }
 

@@ -32,8 +32,8 @@ def timed(fn, reps=3):
     return best, r
 
 
-for variant in (-1, 3):
-    t.tune(query_ilp=variant)
+for variant in (0, 2, 3):
+    t.tune(upsert=variant)
     ins = []
     for rep in range(3):
         t.clear()
@@ -44,8 +44,8 @@ for variant in (-1, 3):
     print(f"insert variant {variant}: {min(ins):.2f} ms  ({n / min(ins) / 1e6:.2f} G/s) bad={bad} occupied={cs[0]}",
           flush=True)
 ref_f, ref_v = None, None
-for ilp in (0, 3, 1, 4):
-    for pol in (0, 1):
+for ilp in (3, 0):
+    for pol in (0, 2):
         t.tune(query_ilp=ilp, l2_policy=pol)
         ms, (f, v) = timed(lambda: t.query_batch(q, check=False))
         if ref_f is None:
