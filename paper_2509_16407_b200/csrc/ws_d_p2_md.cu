@@ -66,6 +66,16 @@ static void p2_md_query(const QueryArgs& a, bool def) {
 #undef WS_QP
       break;
     }
+    case 5: {  // one thread per op, pair-cooperative tag fetches
+      u64 g = (a.n + 255) / 256;
+      g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * 8);
+#define WS_QC(RO, F) k_query_p2md_coop<RO, F><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated)
+      const bool f64 = a.d.tune_l2pol == 2;
+      if (a.ro) { if (f64) WS_QC(true, true); else WS_QC(true, false); }
+      else { if (f64) WS_QC(false, true); else WS_QC(false, false); }
+#undef WS_QC
+      break;
+    }
     case 1: fast_query_q<1>(a); break;
     case 2: fast_query_q<2>(a); break;
     case 8: fast_query_q<8>(a); break;

@@ -406,6 +406,96 @@ __device__ __forceinline__ void red_and_relaxed(u32* p, u32 m) {
   asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" :: "l"(p), "r"(m) : "memory");
 }
 
+// ------------------------------------------------ pair-cooperative loads
+//
+// One thread per op, but the 64-byte tag blocks of lanes 2k and 2k+1 are
+// fetched cooperatively: in the first instruction both lanes load the two
+// halves of op 2k's block, in the second the two halves of op 2k+1's block --
+// one line request per block and still 32 ops per warp.  Each lane then swaps
+// the 16-slot mask half it holds for its partner's op.  Must be called by all
+// 32 lanes (converged); `active` gates the lane's own op.
+__device__ __forceinline__ void half_masks(const u32 (&w)[8], u16 tag, u32& m, u32& z) {
+  const u32 pat = (u32)tag * 0x10001u;
+  m = 0;
+  z = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const u32 mm = __vcmpeq2(w[i], pat), zz = __vcmpeq2(w[i], 0u);
+    m |= ((mm & 1u) | ((mm >> 15) & 2u)) << (2 * i);
+    z |= ((zz & 1u) | ((zz >> 15) & 2u)) << (2 * i);
+  }
+}
+
+template <bool RO, bool F64>
+__device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16 tag, u32& M, u32& Z) {
+  const int half = threadIdx.x & 1;
+  const u64 pb = __shfl_xor_sync(0xFFFFFFFFu, b, 1);
+  const u32 pt = __shfl_xor_sync(0xFFFFFFFFu, (u32)tag, 1);
+  const u32 pa = __shfl_xor_sync(0xFFFFFFFFu, (u32)active, 1);
+  // op A = even lane's op, op B = odd lane's op
+  const u64 bA = half ? pb : b, bB = half ? b : pb;
+  const u16 tA = (u16)(half ? pt : tag), tB = (u16)(half ? tag : pt);
+  const bool aA = half ? pa != 0 : active, aB = half ? active : pa != 0;
+  u32 wA[8], wB[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) { wA[i] = 0xFFFFFFFFu; wB[i] = 0xFFFFFFFFu; }
+  const u16* pA = d.tags + bA * 32 + half * 16;
+  const u16* pB = d.tags + bB * 32 + half * 16;
+  if (aA) {
+    if (F64) { if (RO) ld_tags32_ro64(pA, wA); else ld_tags32_64(pA, wA); }
+    else { if (RO) ld_tags32_ro(pA, wA); else ld_tags32(pA, wA); }
+  }
+  if (aB) {
+    if (F64) { if (RO) ld_tags32_ro64(pB, wB); else ld_tags32_64(pB, wB); }
+    else { if (RO) ld_tags32_ro(pB, wB); else ld_tags32(pB, wB); }
+  }
+  u32 mA, zA, mB, zB;
+  half_masks(wA, tA, mA, zA);
+  half_masks(wB, tB, mB, zB);
+  // even lane holds A-lo (needs A-hi from odd); odd holds B-hi (needs B-lo)
+  const u32 rm = __shfl_xor_sync(0xFFFFFFFFu, half ? mA : mB, 1);
+  const u32 rz = __shfl_xor_sync(0xFFFFFFFFu, half ? zA : zB, 1);
+  if (!half) { M = mA | (rm << 16); Z = zA | (rz << 16); }
+  else { M = rm | (mB << 16); Z = rz | (zB << 16); }
+}
+
+// One thread per query, pair-cooperative tag fetches (see coop_masks).
+template <bool RO, bool F64>
+__global__ void __launch_bounds__(256) k_query_p2md_coop(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
+                                                         u8* found, int conc_erase, int gated) {
+  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  const u32 te0 = ld_u32_relaxed(d.state);
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  // the loop runs warp-uniformly: the bound is the warp's first index
+  for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n; base += stride) {
+    const u64 i = base + (threadIdx.x & 31);
+    const bool act = i < n;
+    const u64 key = act ? __ldg(keys + i) : 0;
+    const u64 h0 = mix64(key ^ d.seeds[0]);
+    const u64 b0 = d.nbm(h0 >> 16);
+    const u16 t = (u16)(h0 & 0xFFFF);
+    const u16 tag = t ? t : (u16)1;
+    u32 M, Z;
+    coop_masks<RO, F64>(d, act, b0, tag, M, Z);
+    u64 val = 0;
+    bool hit = act && M && pair_confirm<RO, F64>(d, b0, M, key, val) >= 0;
+    bool te = te0 != 0;
+    if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
+    const int zc = __popc(Z);
+    const int used0 = 32 - (zc < d.zcc ? zc : d.zcc);
+    const u64 b1 = d.nbm(mix64(key ^ d.seeds[1]) >> 16);
+    const bool need1 = act && !hit && !(Z && !te && used0 < d.shortcut) && b1 != b0;
+    if (__any_sync(0xFFFFFFFFu, need1)) {
+      coop_masks<RO, F64>(d, need1, b1, tag, M, Z);
+      if (need1 && M) hit = pair_confirm<RO, F64>(d, b1, M, key, val) >= 0;
+    }
+    if (act) {
+      if (found) found[i] = hit;
+      if (vout) vout[i] = hit ? val : 0;
+    }
+  }
+}
+
 template <bool F64>
 __global__ void __launch_bounds__(256) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, int merge,
@@ -431,70 +521,73 @@ __global__ void __launch_bounds__(256) k_upsert_p2md_rounds(Dev d, const u64* __
     u8 st = 0;
     unsigned backoff = 64;
     while (__any_sync(0xFFFFFFFFu, pending)) {
-      bool hold0 = false, hold1 = false;
-      if (pending) {
-        hold0 = try_lock_bucket(d.locks, b0);
-        if (hold0) {
-          u32 M0, Z0;
-          tag_masks_t<F64>(d, b0, tag, M0, Z0);
-          u64 old;
-          int j = M0 ? pair_confirm<false, F64>(d, b0, M0, key, old) : -1;
-          if (j >= 0) {
-            st_cell(d.cells + 2 * (b0 * 32 + j), key, apply_merge(merge, old, val));
-            st = S_UPDATED;
-            pending = false;
+      // phase 1: try-lock the primary (never blocks)
+      const bool hold0 = pending && try_lock_bucket(d.locks, b0);
+      // phase 2: primary tag blocks, one request per op
+      u32 M0, Z0;
+      coop_masks<false, F64>(d, hold0, b0, tag, M0, Z0);
+      bool hold1 = false, need1 = false, decided = false;
+      u64 old;
+      int used0 = 0;
+      if (hold0) {
+        const int j = M0 ? pair_confirm<false, F64>(d, b0, M0, key, old) : -1;
+        if (j >= 0) {
+          st_cell(d.cells + 2 * (b0 * 32 + j), key, apply_merge(merge, old, val));
+          st = S_UPDATED;
+          pending = false;
+        } else {
+          bool te = te0 != 0;
+          if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
+          const int zc0 = __popc(Z0);
+          used0 = 32 - (zc0 < d.zcc ? zc0 : d.zcc);
+          if ((te || used0 >= d.shortcut) && b1 != b0) {
+            hold1 = try_lock_bucket(d.locks, b1);
+            need1 = hold1;  // a failed try-lock retries the whole op next round
           } else {
-            bool te = te0 != 0;
-            if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
-            const int zc0 = __popc(Z0);
-            const int used0 = 32 - (zc0 < d.zcc ? zc0 : d.zcc);
-            u64 target = b0;
-            u32 Zt = Z0;
-            bool decided = true;
-            if ((te || used0 >= d.shortcut) && b1 != b0) {
-              hold1 = try_lock_bucket(d.locks, b1);
-              if (!hold1) {
-                decided = false;  // retry the whole op next round
-              } else {
-                u32 M1, Z1;
-                tag_masks_t<F64>(d, b1, tag, M1, Z1);
-                j = M1 ? pair_confirm<false, F64>(d, b1, M1, key, old) : -1;
-                if (j >= 0) {
-                  st_cell(d.cells + 2 * (b1 * 32 + j), key, apply_merge(merge, old, val));
-                  st = S_UPDATED;
-                  pending = false;
-                  decided = false;
-                } else {
-                  const int zc1 = __popc(Z1);
-                  const int used1 = 32 - (zc1 < d.zcc ? zc1 : d.zcc);
-                  const bool prim = used0 <= used1;  // ties go to the primary
-                  target = prim ? b0 : b1;
-                  Zt = prim ? Z0 : Z1;
-                  if (!Zt) { target = prim ? b1 : b0; Zt = prim ? Z1 : Z0; }
-                }
-              }
-            }
-            if (decided) {
-              if (!Zt) {
-                st = S_FULL;
-              } else {
-                const u64 slot = target * 32 + (__ffs(Zt) - 1);
-                if (conc_erase) fence_acq_rel();
-                st_cell(d.cells + 2 * slot, key, val);
-                st_tag(d.tags + slot, tag);
-                st = S_INSERTED;
-              }
-              pending = false;
-            }
+            decided = true;  // shortcut (or b1 == b0): the primary it is
           }
         }
       }
+      // phase 3: alternate tag blocks of the lanes that need them
+      u32 M1 = 0, Z1 = 0;
+      if (__any_sync(0xFFFFFFFFu, need1)) coop_masks<false, F64>(d, need1, b1, tag, M1, Z1);
+      u64 target = b0;
+      u32 Zt = Z0;
+      if (need1) {
+        const int j = M1 ? pair_confirm<false, F64>(d, b1, M1, key, old) : -1;
+        if (j >= 0) {
+          st_cell(d.cells + 2 * (b1 * 32 + j), key, apply_merge(merge, old, val));
+          st = S_UPDATED;
+          pending = false;
+        } else {
+          const int zc1 = __popc(Z1);
+          const int used1 = 32 - (zc1 < d.zcc ? zc1 : d.zcc);
+          const bool prim = used0 <= used1;  // ties go to the primary
+          target = prim ? b0 : b1;
+          Zt = prim ? Z0 : Z1;
+          if (!Zt) { target = prim ? b1 : b0; Zt = prim ? Z1 : Z0; }
+          decided = true;
+        }
+      }
+      if (decided) {
+        if (!Zt) {
+          st = S_FULL;
+        } else {
+          const u64 slot = target * 32 + (__ffs(Zt) - 1);
+          if (conc_erase) fence_acq_rel();
+          st_cell(d.cells + 2 * slot, key, val);
+          st_tag(d.tags + slot, tag);
+          st = S_INSERTED;
+        }
+        pending = false;
+      }
+      // phase 4: one MEMBAR for the warp, then relaxed releases
       __syncwarp();
-      fence_acq_rel();  // one MEMBAR per warp-round: publications before the unlocks
+      fence_acq_rel();
       if (hold1) red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
       if (hold0) red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
       if (pending) {
-        __nanosleep(backoff + 8 * lane);
+        __nanosleep(backoff + 8 * (threadIdx.x & 31));
         if (backoff < 4096) backoff <<= 1;
       }
     }

@@ -44,7 +44,7 @@ for variant in (0, 2, 3):
     print(f"insert variant {variant}: {min(ins):.2f} ms  ({n / min(ins) / 1e6:.2f} G/s) bad={bad} occupied={cs[0]}",
           flush=True)
 ref_f, ref_v = None, None
-for ilp in (3, 0):
+for ilp in (3, 5):
     for pol in (0, 2):
         t.tune(query_ilp=ilp, l2_policy=pol)
         ms, (f, v) = timed(lambda: t.query_batch(q, check=False))

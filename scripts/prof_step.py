@@ -19,11 +19,15 @@ ap.add_argument("--log2-slots", type=int, default=28)
 ap.add_argument("--design", default="p2_md")
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--load", type=float, default=0.9)
+ap.add_argument("--upsert", type=int, default=None)
+ap.add_argument("--query", type=int, default=None)
 a = ap.parse_args()
 
 slots = 1 << a.log2_slots
 n = int(slots * a.load)
 t = make_table(TableConfig(design=a.design, capacity_slots=slots, seed=42))
+if a.design == "p2_md":
+    t.tune(query_ilp=a.query, upsert=a.upsert)
 kh = gen_uniform_keys(42, n)
 keys = torch.from_numpy(kh.view(np.int64)).cuda()
 vals = keys & 0xFFFF
