@@ -144,11 +144,13 @@ WS_API int ws_export_raw(ws_table *t, uint64_t *words, uint64_t nwords, uint16_t
 WS_API int ws_info(ws_table *t, ws_info_t *info);
 
 /* performance knobs (no semantic effect) */
-#define WS_TUNE_QUERY_ILP 1 /* P2-MD kernel variant: 3 = lane-pair tiles (default), 1/2/4/8 = lookups
-                               per thread, 0 = generic kernels, -1 = generic kernels for upserts too */
+#define WS_TUNE_QUERY_ILP 1 /* P2-MD query kernel: 5 = one thread per op with pair-cooperative tag
+                               fetches (default), 3 = lane-pair tiles, 1/2/4/8 = lookups per thread,
+                               0 = generic kernel */
 #define WS_TUNE_L2_POLICY 2 /* 1: tag loads L2 evict_last, cell loads evict_first; 2: 64-byte L2 fills */
 #define WS_TUNE_UPSERT 3    /* P2-MD upsert: 0 one thread per op, 1 lane-pair tiles,
-                               2 warp-synchronous lock rounds, 3 rounds + 64-byte L2 fills */
+                               2 warp-synchronous lock rounds, 3 rounds + 64-byte L2 fills (default) */
+#define WS_TUNE_OCCUPANCY 4 /* tuned kernels: request >= value CTAs/SM from ptxas (0 = compiler choice) */
 WS_API int ws_tune(ws_table *t, int knob, int value);
 
 WS_API const char *ws_strerror(int code);

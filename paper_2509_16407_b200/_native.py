@@ -33,6 +33,7 @@ EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_e
 WS_TUNE_QUERY_ILP = 1
 WS_TUNE_L2_POLICY = 2
 WS_TUNE_UPSERT = 3
+WS_TUNE_OCCUPANCY = 4
 
 
 class WsConfig(C.Structure):

@@ -420,9 +420,10 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.lock_elided = c.design == D_UNSAFE;
   d.line_bytes = c.line_bytes;
   d.wpn = 2 * c.bucket_size + 2;
-  d.tune_qilp = 3;
-  d.tune_l2pol = 0;
-  d.tune_upsert = 0;
+  d.tune_qilp = 5;
+  d.tune_l2pol = 2;
+  d.tune_upsert = 3;
+  d.tune_occ = 0;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };
   if (c.design == D_CHAINING) {
@@ -718,6 +719,9 @@ int ws_tune(ws_table* t, int knob, int value) {
     case WS_TUNE_L2_POLICY:
       if (value < 0 || value > 2) return WS_ERR_ARG;
       t->d.tune_l2pol = value;
+      return WS_OK;
+    case WS_TUNE_OCCUPANCY:
+      t->d.tune_occ = value;
       return WS_OK;
     case WS_TUNE_UPSERT:
       if (value < 0 || value > 3) return WS_ERR_ARG;

@@ -40,12 +40,15 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
     g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
-    if (a.d.tune_upsert == 3)
-      k_upsert_p2md_rounds<true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status,
-                                                               a.conc_erase, a.gated);
-    else
-      k_upsert_p2md_rounds<false><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status,
-                                                                a.conc_erase, a.gated);
+#define WS_UR(F, MB) k_upsert_p2md_rounds<F, MB><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, \
+                                                   a.uop >> 4, a.status, a.conc_erase, a.gated)
+    const bool f64 = a.d.tune_upsert == 3;
+    switch (a.d.tune_occ) {
+      case 5: if (f64) WS_UR(true, 5); else WS_UR(false, 5); break;
+      case 6: if (f64) WS_UR(true, 6); else WS_UR(false, 6); break;
+      default: if (f64) WS_UR(true, 1); else WS_UR(false, 1); break;
+    }
+#undef WS_UR
     return;
   }
   if (def) launch_ops_t<D_P2_MD, 32>(a); else launch_ops_t<D_P2_MD, 0>(a);
@@ -69,10 +72,13 @@ static void p2_md_query(const QueryArgs& a, bool def) {
     case 5: {  // one thread per op, pair-cooperative tag fetches
       u64 g = (a.n + 255) / 256;
       g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * 8);
-#define WS_QC(RO, F) k_query_p2md_coop<RO, F><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated)
+#define WS_QC(RO, F, MB) k_query_p2md_coop<RO, F, MB><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase, a.gated)
+#define WS_QC2(MB) \
+  if (a.ro) { if (f64) WS_QC(true, true, MB); else WS_QC(true, false, MB); } \
+  else { if (f64) WS_QC(false, true, MB); else WS_QC(false, false, MB); }
       const bool f64 = a.d.tune_l2pol == 2;
-      if (a.ro) { if (f64) WS_QC(true, true); else WS_QC(true, false); }
-      else { if (f64) WS_QC(false, true); else WS_QC(false, false); }
+      if (a.d.tune_occ == 8) { WS_QC2(8) } else { WS_QC2(1) }
+#undef WS_QC2
 #undef WS_QC
       break;
     }

@@ -460,8 +460,8 @@ __device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16
 }
 
 // One thread per query, pair-cooperative tag fetches (see coop_masks).
-template <bool RO, bool F64>
-__global__ void __launch_bounds__(256) k_query_p2md_coop(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
+template <bool RO, bool F64, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                          u8* found, int conc_erase, int gated) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
   const u32 te0 = ld_u32_relaxed(d.state);
@@ -496,8 +496,8 @@ __global__ void __launch_bounds__(256) k_query_p2md_coop(Dev d, const u64* __res
   }
 }
 
-template <bool F64>
-__global__ void __launch_bounds__(256) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
+template <bool F64, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, int merge,
                                                             u8* status, int conc_erase, int gated) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;

@@ -43,7 +43,8 @@ struct Dev {
   int design, bs, md, shortcut, zcc, probe_cap, ways, depth, phased, lock_elided, line_bytes, wpn;
   int tune_qilp;   // lookups per thread in the tuned query kernel (1, 2, 4)
   int tune_l2pol;  // 1: tag loads evict_last, cell loads evict_first
-  int tune_upsert; // P2-MD upsert kernel: 0 generic one-thread-per-op, 1 lane pair
+  int tune_upsert; // P2-MD upsert kernel: 0 generic one-thread-per-op, 1 lane pair, 2/3 rounds
+  int tune_occ;    // minimum resident CTAs per SM requested from ptxas (register cap)
 };
 
 __device__ __forceinline__ u64 apply_merge(int m, u64 old, u64 nv) {

@@ -549,8 +549,10 @@ class HashTable:
         return {"slot_engine": self.slot_engine, "wide_atomic": True,
                 "device": f"cuda:{self.device.index}", "arch": "sm_100a"}
 
-    def tune(self, query_ilp=None, l2_policy=None, upsert=None):
+    def tune(self, query_ilp=None, l2_policy=None, upsert=None, occupancy=None):
         """Performance knobs of the tuned P2-MD path (no semantic effect)."""
+        if occupancy is not None:
+            self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_OCCUPANCY, int(occupancy)))
         if upsert is not None:
             self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_UPSERT, int(upsert)))
         if query_ilp is not None:

@@ -53,3 +53,16 @@ for ilp in (3, 5):
         ok = torch.equal(f, ref_f) and torch.equal(v.view(torch.int64), ref_v.view(torch.int64))
         print(f"query ilp={ilp} pol={pol}: {ms:.2f} ms ({n / ms / 1e6:.2f} G/s) same={ok} hits={int(f.sum())}",
               flush=True)
+
+for occ in (0, 5, 6):
+    t.tune(upsert=3, occupancy=occ)
+    best = 1e9
+    for rep in range(3):
+        t.clear()
+        ms, st = timed(lambda: t.upsert_batch(keys.view(torch.uint64), vals.view(torch.uint64), check=False), 1)
+        best = min(best, ms)
+    print(f"insert rounds occ={occ}: {best:.2f} ms ({n / best / 1e6:.2f} G/s) bad={int((st != 0).sum())}", flush=True)
+for occ in (0, 8):
+    t.tune(query_ilp=5, l2_policy=2, occupancy=occ)
+    ms, (f, v) = timed(lambda: t.query_batch(q, check=False))
+    print(f"query coop occ={occ}: {ms:.2f} ms ({n / ms / 1e6:.2f} G/s) hits={int(f.sum())}", flush=True)
