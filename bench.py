@@ -32,12 +32,21 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Mops/s insert+query at 0.9 load, 1/2/4/8 B200; % HBM random-access roofline"
 UNIT = "Mops/s"
-# algorithmic HBM bytes per op: random table traffic
-# from SURVEY 8(d) plus the streaming batch I/O (key 8 + value 8 + status 1)
-INSERT_TABLE_B = 175.0
+# Algorithmic HBM bytes per op, 32-byte sectors:
+#   insert (0 -> 0.9 fill): primary tag block 64 + alternate tag block 64 x 0.232
+#     (fraction of non-shortcut inserts, oracle-measured) + cell sector write 32
+#     + tag sector write 32 = 142.8; batch I/O key 8 + value 8 + status 1 = 17
+#   query (50/50 at 0.9): positive 64 + 32 (+ 64 x 0.124 alternate) = 104,
+#     negative 64 + 64 = 128 -> 116; batch I/O key 8 + found 1 + value 8 = 17
+INSERT_TABLE_B = 64 + 64 * 0.232 + 32 + 32
 QUERY_TABLE_B = 116.0
 INSERT_IO_B = 17.0
 QUERY_IO_B = 17.0
+# L2-missing line requests per op (what the B200 random-access ceiling counts):
+# insert = primary tags 1 + alternate tags 0.232 + cell write 1; query =
+# 0.5 x (1 + 1 + 0.124) + 0.5 x 2 (positive / negative)
+INSERT_REQ = 2.232
+QUERY_REQ = 2.062
 
 
 def parse():
@@ -292,10 +301,14 @@ def run_ours(args, rank, world):
     ins_gbs = ins_bytes / (ms_ins / 1000) / 1e9
     qry_gbs = qry_bytes / (ms_qry / 1000) / 1e9
     traffic = None
+    ceiling = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("insert_bytes_per_launch")
+            pj = json.load(open(prof))
+            if pj.get("log2_slots") == args.log2_slots and pj.get("design") == args.design:
+                traffic = pj.get("insert_dram_bytes_per_launch")
+            ceiling = pj.get("random_request_ceiling_g_per_s")
         except Exception:  # noqa: BLE001
             traffic = None
     cpu = None
@@ -319,13 +332,21 @@ def run_ours(args, rank, world):
             "insert_mops": round(n / ms_ins / 1e3, 1), "query_mops": round(n / ms_qry / 1e3, 1),
         },
         "roofline": {
-            "bound": "hbm", "kernel": "k_ops<P2_MD> (upsert)", "achieved": round(ins_gbs, 1),
+            "bound": "hbm", "kernel": "k_upsert_p2md_rounds", "achieved": round(ins_gbs, 1),
             "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ins_gbs / peak, 4),
             "traffic": traffic,
             "algorithmic_bytes_per_op": INSERT_TABLE_B + INSERT_IO_B,
-            "query_kernel": {"kernel": "k_query<P2_MD>", "achieved": round(qry_gbs, 1),
+            "query_kernel": {"kernel": "k_query_p2md_coop", "achieved": round(qry_gbs, 1),
                              "frac": round(qry_gbs / peak, 4),
                              "algorithmic_bytes_per_op": QUERY_TABLE_B + QUERY_IO_B},
+            "random_access": {
+                "unit": "G L2-miss line requests/s",
+                "ceiling": ceiling,
+                "ceiling_source": "scripts/gather_bench.cu (profiles/ncu_traffic.json)",
+                "insert_requests_per_op": INSERT_REQ, "query_requests_per_op": QUERY_REQ,
+                "insert_achieved": round(n * INSERT_REQ / ms_ins / 1e6, 2),
+                "query_achieved": round(n * QUERY_REQ / ms_qry / 1e6, 2),
+            },
         },
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
