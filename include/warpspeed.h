@@ -26,6 +26,8 @@
  *   ws_export_raw             slots.key_at / tags.get / arena words (test introspection)
  *   ws_info                   storage_report / arena.next_node / _tombstones_ever
  *   ws_tune                   (new) performance knobs, no semantic effect
+ *   ws_partition/ws_unpermute (new) owner routing of the hash-sharded multi-GPU table
+ *                             (the reference has no multi-GPU layer)
  *   ws_strerror               exception messages (InvalidKeyError / ConfigError)
  *
  * Semantics: a batch is a set of operations that execute concurrently on the
@@ -152,6 +154,17 @@ WS_API int ws_info(ws_table *t, ws_info_t *info);
                                2 warp-synchronous lock rounds, 3 rounds + 64-byte L2 fills (default) */
 #define WS_TUNE_OCCUPANCY 4 /* tuned kernels: request >= value CTAs/SM from ptxas (0 = compiler choice) */
 WS_API int ws_tune(ws_table *t, int knob, int value);
+
+/* hash-sharded multi-GPU routing (device pointers): split a batch into
+ * 2^log2_parts per-owner contiguous segments, owner = top log2_parts bits of
+ * mix64(key ^ seed0); perm[j] = source index of output j; counts[p] = segment
+ * sizes.  vals / ops / out_vals / out_ops may be NULL.  n < 2^32. */
+WS_API int ws_partition(const uint64_t *keys, const uint64_t *vals, const uint8_t *ops, uint64_t n,
+                        uint64_t seed0, int log2_parts, uint64_t *out_keys, uint64_t *out_vals,
+                        uint8_t *out_ops, uint32_t *perm, uint64_t *counts, void *stream);
+/* out[perm[j]] = in[j] for elements of 1, 4 or 8 bytes (device pointers) */
+WS_API int ws_unpermute(const void *in, const uint32_t *perm, uint64_t n, int elem_bytes, void *out,
+                        void *stream);
 
 WS_API const char *ws_strerror(int code);
 

@@ -29,7 +29,7 @@ WS_F_SERIAL = 4
 EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_erase", "ws_mixed",
            "ws_locate", "ws_probe_counts", "ws_occupied", "ws_export_items",
            "ws_duplicate_scan", "ws_checksum", "ws_export_raw", "ws_info", "ws_tune",
-           "ws_strerror")
+           "ws_partition", "ws_unpermute", "ws_strerror")
 WS_TUNE_QUERY_ILP = 1
 WS_TUNE_L2_POLICY = 2
 WS_TUNE_UPSERT = 3
@@ -90,6 +90,8 @@ def load():
         lib.ws_export_raw.argtypes = [vp, vp, u64, vp, vp]
         lib.ws_info.argtypes = [vp, C.POINTER(WsInfo)]
         lib.ws_tune.argtypes = [vp, i32, i32]
+        lib.ws_partition.argtypes = [vp, vp, vp, u64, u64, i32, vp, vp, vp, vp, vp, vp]
+        lib.ws_unpermute.argtypes = [vp, vp, u64, i32, vp, vp]
         lib.ws_strerror.argtypes = [i32]
         lib.ws_strerror.restype = C.c_char_p
         for name in EXPORTS:

@@ -1,0 +1,192 @@
+"""Hash-sharded table over the ranks of a torch.distributed process group.
+
+One logical table of ``config.capacity_slots`` slots is split into one local
+device table per rank (``capacity_slots / world`` slots each).  The owner of a
+key is the top log2(world) bits of its primary hash ``mix64(k ^ seed0)``; the
+local table indexes bucket bits 16..16+log2(nb), so owner and bucket are
+independent.  The reference has no multi-GPU layer;
+every batch op here is:
+
+    partition by owner (ws_partition)  ->  all_to_all_single of the keys
+    (+ values / op bytes)  ->  local batch op  ->  reverse all_to_all_single
+    of the results  ->  scatter back to the caller's order (ws_unpermute)
+
+Each rank passes its own batch; results come back for that batch.  With one
+rank the exchange is skipped entirely.  The process group is the caller's
+(NCCL over NVLink for device tensors; the CPU tests drive the same routing
+logic over gloo with an injected CPU router and local table).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+
+from .core import ConfigError, TableConfig, validate_config
+
+
+class DeviceRouter:
+    """Owner partition / result scatter on the GPU (libwarpspeed kernels)."""
+
+    def __init__(self, seed0: int, log2_parts: int):
+        from . import _native
+        self._lib = _native.load()
+        self.seed0 = seed0
+        self.log2 = log2_parts
+
+    def partition(self, keys, vals=None, ops=None):
+        import torch
+        n = keys.numel()
+        if not keys.is_cuda:
+            raise RuntimeError("sharded batches must be CUDA tensors")
+        parts = 1 << self.log2
+        ok = torch.empty_like(keys)
+        ov = torch.empty_like(vals) if vals is not None else None
+        oo = torch.empty_like(ops) if ops is not None else None
+        perm = torch.empty(n, dtype=torch.int32, device=keys.device)
+        counts = torch.empty(parts, dtype=torch.int64, device=keys.device)
+        s = torch.cuda.current_stream(keys.device).cuda_stream
+        rc = self._lib.ws_partition(keys.data_ptr(), vals.data_ptr() if vals is not None else None,
+                                    ops.data_ptr() if ops is not None else None, n, self.seed0,
+                                    self.log2, ok.data_ptr(), ov.data_ptr() if ov is not None else None,
+                                    oo.data_ptr() if oo is not None else None, perm.data_ptr(),
+                                    counts.data_ptr(), s)
+        if rc:
+            raise RuntimeError(f"ws_partition failed ({rc})")
+        return ok, ov, oo, perm, counts
+
+    def unpermute(self, res, perm):
+        import torch
+        out = torch.empty_like(res)
+        s = torch.cuda.current_stream(res.device).cuda_stream
+        rc = self._lib.ws_unpermute(res.data_ptr(), perm.data_ptr(), res.numel(), res.element_size(),
+                                    out.data_ptr(), s)
+        if rc:
+            raise RuntimeError(f"ws_unpermute failed ({rc})")
+        return out
+
+
+class ShardedTable:
+    """A table spread over all ranks of ``group``; batched ops only."""
+
+    def __init__(self, config: TableConfig, group=None, local_table=None, router=None, **table_kw):
+        import torch.distributed as dist
+        cfg = validate_config(config)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if self.world & (self.world - 1):
+            raise ConfigError([f"world size {self.world} is not a power of two"])
+        self.log2 = self.world.bit_length() - 1
+        if cfg.capacity_slots % (self.world * cfg.bucket_size):
+            raise ConfigError([f"capacity_slots {cfg.capacity_slots} does not split into "
+                               f"{self.world} shards of whole buckets"])
+        self.config = cfg
+        self.local_config = dataclasses.replace(cfg, capacity_slots=cfg.capacity_slots // self.world)
+        if local_table is None:
+            from .tables import make_table
+            local_table = make_table(self.local_config, **table_kw)
+        self.local = local_table
+        self.seed0 = cfg.hash_family().seeds[0]
+        self.router = router if router is not None else DeviceRouter(self.seed0, self.log2)
+
+    # --------------------------------------------------------------- exchange
+    def _counts(self, send_counts):
+        import torch
+        import torch.distributed as dist
+        recv = torch.empty_like(send_counts)
+        dist.all_to_all_single(recv, send_counts, group=self.group)
+        return recv
+
+    def _a2a(self, t, recv_splits, send_splits):
+        import torch
+        import torch.distributed as dist
+        view = t.view(torch.int64) if t.dtype == torch.uint64 else t
+        out = torch.empty(sum(recv_splits), dtype=view.dtype, device=t.device)
+        dist.all_to_all_single(out, view, recv_splits, send_splits, group=self.group)
+        return out.view(t.dtype)
+
+    def _route(self, keys, vals=None, ops=None):
+        pk, pv, po, perm, counts = self.router.partition(keys, vals, ops)
+        rcounts = self._counts(counts)
+        send = counts.cpu().tolist()
+        recv = rcounts.cpu().tolist()
+        rk = self._a2a(pk, recv, send)
+        rv = self._a2a(pv, recv, send) if pv is not None else None
+        ro = self._a2a(po, recv, send) if po is not None else None
+        return rk, rv, ro, perm, send, recv
+
+    def _back(self, res, perm, send, recv):
+        out = self._a2a(res, send, recv)
+        return self.router.unpermute(out, perm)
+
+    # ----------------------------------------------------------------- ops
+    def upsert_batch(self, keys, values, merge=None, check=True):
+        if self.world == 1:
+            return self.local.upsert_batch(keys, values, merge=merge, check=check)
+        rk, rv, _ro, perm, send, recv = self._route(keys, values)
+        st = self.local.upsert_batch(rk, rv, merge=merge, check=check)
+        return self._back(st, perm, send, recv)
+
+    def query_batch(self, keys, check=True):
+        if self.world == 1:
+            return self.local.query_batch(keys, check=check)
+        rk, _rv, _ro, perm, send, recv = self._route(keys)
+        found, vals = self.local.query_batch(rk, check=check)
+        import torch
+        found = self._back(found.to(torch.uint8), perm, send, recv)
+        vals = self._back(vals, perm, send, recv)
+        return found.bool(), vals
+
+    def erase_batch(self, keys, check=True):
+        if self.world == 1:
+            return self.local.erase_batch(keys, check=check)
+        rk, _rv, _ro, perm, send, recv = self._route(keys)
+        import torch
+        found = self.local.erase_batch(rk, check=check)
+        return self._back(found.to(torch.uint8), perm, send, recv).bool()
+
+    def mixed_batch(self, ops, keys, values=None, check=True):
+        import torch
+        if values is None:
+            values = torch.zeros(keys.numel(), dtype=keys.dtype, device=keys.device)
+        if self.world == 1:
+            return self.local.mixed_batch(ops, keys, values, check=check)
+        rk, rv, ro, perm, send, recv = self._route(keys, values, ops)
+        st, vo = self.local.mixed_batch(ro, rk, rv, check=check)
+        return self._back(st, perm, send, recv), self._back(vo, perm, send, recv)
+
+    # --------------------------------------------------- collective summaries
+    def _gather(self, vals):
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return [list(vals)]
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v for v in vals], dtype=torch.int64,
+                         device=dev)
+        outs = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(outs, t, group=self.group)
+        return [[int(x) & ((1 << 64) - 1) for x in o.cpu().tolist()] for o in outs]
+
+    def checksum(self):
+        """(occupied, Σkeys, Σvalues, ⊕ mix64(k ^ mix64(v))) over all shards (mod 2^64)."""
+        parts = self._gather(self.local.checksum())
+        m = (1 << 64) - 1
+        c = sk = sv = x = 0
+        for p in parts:
+            c += p[0]
+            sk = (sk + p[1]) & m
+            sv = (sv + p[2]) & m
+            x ^= p[3]
+        return c, sk, sv, x
+
+    def occupied_count(self):
+        return self.checksum()[0]
+
+    def duplicate_count(self):
+        # a key lives on exactly one owner, so duplicates are shard-local
+        return sum(p[0] for p in self._gather([self.local.duplicate_count()]))
+
+    def clear(self):
+        self.local.clear()

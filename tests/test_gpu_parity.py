@@ -302,3 +302,43 @@ def test_p2md_2pow28_fill_and_query_properties():
     found, _ = t.query_batch(miss)
     assert int(found.sum()) == 0
     assert t.duplicate_count() == 0
+
+
+# ----------------------------------------------------- sharding kernels
+
+@pytest.mark.parametrize("log2", [0, 1, 3, 6])
+def test_partition_kernel_matches_owner_rule(log2):
+    """ws_partition splits a batch into per-owner segments (owner = top log2
+    bits of mix64(k ^ seed0)), perm maps outputs to sources, and ws_unpermute
+    inverts it -- the routing the multi-GPU table does around all_to_all."""
+    from paper_2509_16407_b200.sharded import DeviceRouter
+    from paper_2509_16407_b200.workload import mix64_np
+    seed0 = 0xBDD732262FEB6E95
+    keys = _keys(21, 300_001)
+    vals = keys ^ np.uint64(5)
+    ops = (np.arange(len(keys)) % 3).astype(np.uint8)
+    r = DeviceRouter(seed0, log2)
+    pk, pv, po, perm, counts = r.partition(_cuda(keys), _cuda(vals), _cuda(ops))
+    pk, pv, po, perm, counts = _np(pk), _np(pv), _np(po), perm.cpu().numpy(), counts.cpu().numpy()
+    own = (np.zeros(len(keys), dtype=np.int64) if log2 == 0 else
+           (mix64_np(keys ^ np.uint64(seed0)) >> np.uint64(64 - log2)).astype(np.int64))
+    np.testing.assert_array_equal(counts, np.bincount(own, minlength=1 << log2))
+    assert sorted(perm.tolist()) == list(range(len(keys)))
+    np.testing.assert_array_equal(pk, keys[perm])
+    np.testing.assert_array_equal(pv, vals[perm])
+    np.testing.assert_array_equal(po, ops[perm])
+    seg = np.repeat(np.arange(1 << log2), counts)
+    np.testing.assert_array_equal(own[perm], seg)
+    back = r.unpermute(_cuda(pk), torch.from_numpy(perm.astype(np.int32)).cuda())
+    np.testing.assert_array_equal(_np(back), keys)
+
+
+def test_sharded_table_single_rank_is_the_local_table():
+    from paper_2509_16407_b200.core import TableConfig
+    from paper_2509_16407_b200.sharded import ShardedTable
+    st = ShardedTable(TableConfig(design="p2_md", capacity_slots=1 << 16, seed=3))
+    keys = _keys(2, 50_000)
+    assert (_np(st.upsert_batch(_cuda(keys), _cuda(keys))) == 0).all()
+    f, v = st.query_batch(_cuda(keys))
+    assert bool(f.all())
+    assert st.checksum()[0] == 50_000
