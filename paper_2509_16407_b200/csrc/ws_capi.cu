@@ -135,8 +135,8 @@ struct ws_table {
   u64 cell_words;
   u64 lock_words;
   u64* h_pin;  // pinned scratch (64 words)
-  cudaStream_t s_aux;
-  cudaEvent_t ev_a, ev_b;
+  cudaStream_t s_aux, s_in;
+  cudaEvent_t ev_a, ev_b, ev_in;
 };
 
 namespace {
@@ -254,53 +254,96 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   return rc;
 }
 
-// Host-buffer batches: stage through device memory.  Inputs are copied H2D in
-// full (the whole batch is validated before any mutation), then the batch runs
-// in chunks whose results stream back D2H on an auxiliary stream while the
-// next chunk computes.
+// Host-buffer batches: staged through device memory in 4M-op chunks on three
+// streams -- H2D on s_in, validation + kernels on the caller's stream, D2H on
+// s_aux -- so copies in both directions overlap compute.  Queries never
+// mutate, so each chunk is queried as soon as it lands and an invalid key is
+// reported after the fact.  Mutating batches must be validated in full before
+// the first mutation: all chunks are copied and validated (overlapped), one
+// sync reads the verdict, then compute and D2H overlap chunk by chunk.
 int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                bool query_only) {
   if (!n) return WS_OK;
   const bool k_dev = is_device_ptr(keys), v_dev = is_device_ptr(vals), o_dev = is_device_ptr(ops);
   const bool st_dev = is_device_ptr(status), vo_dev = is_device_ptr(vout);
+  const bool hk = !k_dev, hv = vals && !v_dev, ho = ops && !o_dev;
+  const bool hst = status && !st_dev, hvo = vout && !vo_dev;
   char* buf = nullptr;
-  const u64 need = n * (8 * (!k_dev) + 8 * (vals && !v_dev) + (ops && !o_dev) +
-                        (status && !st_dev) + 8 * (vout && !vo_dev)) + 6 * 128;
+  const u64 need = n * (8 * hk + 8 * hv + ho + hst + 8 * hvo) + 6 * 128;
   WS_CK(cudaMallocAsync((void**)&buf, need, s));
   char* p = buf;
   auto carve = [&](u64 bytes) { char* r = p; p += (bytes + 127) & ~127ull; return r; };
-  const u64* dk = keys;
-  const u64* dv = vals;
-  const u8* dops = ops;
-  u8* dst = status;
-  u64* dvo = vout;
-  if (!k_dev) { u64* x = (u64*)carve(8 * n); WS_CK(cudaMemcpyAsync(x, keys, 8 * n, cudaMemcpyHostToDevice, s)); dk = x; }
-  if (vals && !v_dev) { u64* x = (u64*)carve(8 * n); WS_CK(cudaMemcpyAsync(x, vals, 8 * n, cudaMemcpyHostToDevice, s)); dv = x; }
-  if (ops && !o_dev) { u8* x = (u8*)carve(n); WS_CK(cudaMemcpyAsync(x, ops, n, cudaMemcpyHostToDevice, s)); dops = x; }
-  if (status && !st_dev) dst = (u8*)carve(n);
-  if (vout && !vo_dev) dvo = (u64*)carve(8 * n);
-  int rc = validate(t, dk, dops, n, s, true, flags);
-  if (rc) { cudaFreeAsync(buf, s); cudaStreamSynchronize(s); return rc; }
+  const u64* dk = hk ? (const u64*)carve(8 * n) : keys;
+  const u64* dv = hv ? (const u64*)carve(8 * n) : vals;
+  const u8* dops = ho ? (const u8*)carve(n) : ops;
+  u8* dst = hst ? (u8*)carve(n) : status;
+  u64* dvo = hvo ? (u64*)carve(8 * n) : vout;
+  const bool check = !(flags & WS_F_NO_CHECK);
+  if (check) WS_CK(cudaMemsetAsync(t->d.state + 2, 0, 2 * sizeof(u32), s));
+  WS_CK(cudaEventRecord(t->ev_b, s));  // staging allocation visible to s_in / s_aux
+  WS_CK(cudaStreamWaitEvent(t->s_in, t->ev_b, 0));
+  WS_CK(cudaStreamWaitEvent(t->s_aux, t->ev_b, 0));
   const bool chain_up = t->cfg.design == D_CHAINING && has_upsert;
   const u64 chunk = chain_up ? n : (u64)1 << 22;
-  for (u64 off = 0; off < n && rc == WS_OK; off += chunk) {
-    const u64 m = std::min(chunk, n - off);
-    rc = run_device(t, dops ? dops + off : nullptr, uop, dk + off, dv ? dv + off : nullptr, m,
-                    dst ? dst + off : nullptr, dvo ? dvo + off : nullptr, s,
-                    WS_F_NO_CHECK | (flags & WS_F_SERIAL), has_erase,
-                    has_upsert, query_only);
-    if (rc) break;
-    if ((status && !st_dev) || (vout && !vo_dev)) {
-      WS_CK(cudaEventRecord(t->ev_a, s));
-      WS_CK(cudaStreamWaitEvent(t->s_aux, t->ev_a, 0));
-      if (status && !st_dev) WS_CK(cudaMemcpyAsync(status + off, dst + off, m, cudaMemcpyDeviceToHost, t->s_aux));
-      if (vout && !vo_dev) WS_CK(cudaMemcpyAsync(vout + off, dvo + off, 8 * m, cudaMemcpyDeviceToHost, t->s_aux));
+  const u32 sub = WS_F_NO_CHECK | (flags & WS_F_SERIAL);
+  int rc = WS_OK;
+  auto h2d = [&](u64 off, u64 m) -> int {
+    if (hk) WS_CK(cudaMemcpyAsync((void*)(dk + off), keys + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
+    if (hv) WS_CK(cudaMemcpyAsync((void*)(dv + off), vals + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
+    if (ho) WS_CK(cudaMemcpyAsync((void*)(dops + off), ops + off, m, cudaMemcpyHostToDevice, t->s_in));
+    WS_CK(cudaEventRecord(t->ev_in, t->s_in));
+    WS_CK(cudaStreamWaitEvent(s, t->ev_in, 0));
+    if (check) k_validate<<<grid_for(m, kThreads, 4), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
+                                                                         t->d.state);
+    return cuda_err(cudaGetLastError());
+  };
+  auto d2h = [&](u64 off, u64 m) -> int {
+    if (!hst && !hvo) return WS_OK;
+    WS_CK(cudaEventRecord(t->ev_a, s));
+    WS_CK(cudaStreamWaitEvent(t->s_aux, t->ev_a, 0));
+    if (hst) WS_CK(cudaMemcpyAsync(status + off, dst + off, m, cudaMemcpyDeviceToHost, t->s_aux));
+    if (hvo) WS_CK(cudaMemcpyAsync(vout + off, dvo + off, 8 * m, cudaMemcpyDeviceToHost, t->s_aux));
+    return WS_OK;
+  };
+  auto compute = [&](u64 off, u64 m) -> int {
+    return run_device(t, dops ? dops + off : nullptr, uop, dk + off, dv ? dv + off : nullptr, m,
+                      dst ? dst + off : nullptr, dvo ? dvo + off : nullptr, s, sub, has_erase, has_upsert,
+                      query_only);
+  };
+  if (query_only) {
+    for (u64 off = 0; off < n && rc == WS_OK; off += chunk) {
+      const u64 m = std::min(chunk, n - off);
+      rc = h2d(off, m);
+      if (!rc) rc = compute(off, m);
+      if (!rc) rc = d2h(off, m);
+    }
+  } else {
+    for (u64 off = 0; off < n && rc == WS_OK; off += chunk) rc = h2d(off, std::min(chunk, n - off));
+    if (!rc && check) {
+      WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 2, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      WS_CK(cudaStreamSynchronize(s));
+      const u32* c = (const u32*)t->h_pin;
+      if (c[0]) rc = WS_ERR_INVALID_KEY;
+      else if (c[1]) rc = WS_ERR_INVALID_OP;
+    }
+    for (u64 off = 0; off < n && rc == WS_OK; off += chunk) {
+      const u64 m = std::min(chunk, n - off);
+      rc = compute(off, m);
+      if (!rc) rc = d2h(off, m);
     }
   }
   WS_CK(cudaEventRecord(t->ev_b, t->s_aux));
   WS_CK(cudaStreamWaitEvent(s, t->ev_b, 0));
+  WS_CK(cudaEventRecord(t->ev_in, t->s_in));
+  WS_CK(cudaStreamWaitEvent(s, t->ev_in, 0));
   cudaFreeAsync(buf, s);
+  if (query_only && check && rc == WS_OK) {
+    WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 2, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    WS_CK(cudaStreamSynchronize(s));
+    const u32* c = (const u32*)t->h_pin;
+    if (c[0]) rc = WS_ERR_INVALID_KEY;
+  }
   WS_CK(cudaStreamSynchronize(s));
   return rc;
 }
@@ -468,6 +511,17 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   }
   if (cudaMallocHost((void**)&t->h_pin, 64 * 8) != cudaSuccess) return fail(WS_ERR_ALLOC);
   if (cudaStreamCreateWithFlags(&t->s_aux, cudaStreamNonBlocking) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (cudaStreamCreateWithFlags(&t->s_in, cudaStreamNonBlocking) != cudaSuccess) return fail(WS_ERR_CUDA);
+  if (cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
+  {
+    // keep staging / scratch allocations of the stream-ordered pool mapped
+    // between calls instead of returning them to the driver at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      u64 thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   if (cudaEventCreateWithFlags(&t->ev_a, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&t->ev_b, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(WS_ERR_CUDA);
@@ -489,6 +543,8 @@ int ws_destroy(ws_table* t) {
   if (d.bfs_busy) cudaFree(d.bfs_busy);
   if (t->h_pin) cudaFreeHost(t->h_pin);
   if (t->s_aux) cudaStreamDestroy(t->s_aux);
+  if (t->s_in) cudaStreamDestroy(t->s_in);
+  if (t->ev_in) cudaEventDestroy(t->ev_in);
   if (t->ev_a) cudaEventDestroy(t->ev_a);
   if (t->ev_b) cudaEventDestroy(t->ev_b);
   delete t;

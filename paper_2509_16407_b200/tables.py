@@ -391,7 +391,9 @@ class HashTable:
     def _out(self, like_cuda, n, dtype, torch):
         if like_cuda:
             return torch.empty(n, dtype=dtype, device=self.device)
-        return torch.empty(n, dtype=dtype)
+        # host results land in pinned memory so the library's D2H copies are
+        # true async DMA (torch caches pinned blocks across calls)
+        return torch.empty(n, dtype=dtype, pin_memory=n >= 4096)
 
     def upsert_batch(self, keys, values, merge=None, check=True):
         """Concurrent upsert of a batch; returns a uint8 status tensor
