@@ -134,6 +134,12 @@ def _as_u8(x, torch):
     return a, a.ctypes.data, False
 
 
+def _checked_out(t, n, dtype):
+    if t.numel() != n or not t.is_contiguous() or t.element_size() != dtype.itemsize:
+        raise ValueError(f"out tensor must be contiguous with {n} elements of {dtype}")
+    return t
+
+
 class _Slots:
     """Read-only view of the device slot cells (quiescent test introspection,
     mirrors reference sync.py WideSlotArray accessors)."""
@@ -393,29 +399,34 @@ class HashTable:
             return torch.empty(n, dtype=dtype, device=self.device)
         # host results land in pinned memory so the library's D2H copies are
         # true async DMA (torch caches pinned blocks across calls)
-        return torch.empty(n, dtype=dtype, pin_memory=n >= 4096)
+        return torch.empty(n, dtype=dtype, pin_memory=n >= (1 << 20))
 
-    def upsert_batch(self, keys, values, merge=None, check=True):
+    def upsert_batch(self, keys, values, merge=None, check=True, out=None):
         """Concurrent upsert of a batch; returns a uint8 status tensor
-        (0 INSERTED, 1 UPDATED, 2 FULL) on the keys' device."""
+        (0 INSERTED, 1 UPDATED, 2 FULL) on the keys' device (or `out`)."""
         torch = _torch()
         k, kp, kc = _as_u64(keys, torch)
         v, vp, _vc = _as_u64(values, torch)
         if len(v) != len(k):
             raise ValueError("keys and values differ in length")
-        st = self._out(kc, len(k), torch.uint8, torch)
+        st = self._out(kc, len(k), torch.uint8, torch) if out is None else _checked_out(out, len(k), torch.uint8)
         self._dirty()
         fl = _native.WS_F_SYNC_CHECK if check else _native.WS_F_NO_CHECK
         self._check(self._lib.ws_upsert(self._h, kp, vp, len(k), merge_id(merge), st.data_ptr(),
                                         self._stream(), fl))
         return st
 
-    def query_batch(self, keys, check=True):
-        """Lock-free concurrent lookups; returns (found bool, values uint64)."""
+    def query_batch(self, keys, check=True, out=None):
+        """Lock-free concurrent lookups; returns (found bool, values uint64).
+        `out` = (found uint8, values uint64) preallocated results."""
         torch = _torch()
         k, kp, kc = _as_u64(keys, torch)
-        found = self._out(kc, len(k), torch.uint8, torch)
-        vals = self._out(kc, len(k), torch.uint64, torch)
+        if out is None:
+            found = self._out(kc, len(k), torch.uint8, torch)
+            vals = self._out(kc, len(k), torch.uint64, torch)
+        else:
+            found = _checked_out(out[0], len(k), torch.uint8)
+            vals = _checked_out(out[1], len(k), torch.uint64)
         fl = _native.WS_F_SYNC_CHECK if check else _native.WS_F_NO_CHECK
         self._check(self._lib.ws_query(self._h, kp, len(k), vals.data_ptr(), found.data_ptr(),
                                        self._stream(), fl))
