@@ -35,18 +35,21 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
                                                                        a.status, a.conc_erase, a.gated);
     return;
   }
-  if (def && upsert_only && !a.instr && !a.serial && !a.redo && !a.d.phased && !a.d.lock_elided &&
-      a.d.tune_upsert >= 2) {
+  if (def && upsert_only && !a.instr && !a.serial && !a.redo && !a.d.lock_elided && a.d.tune_upsert >= 2) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
     g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
-#define WS_UR(F, MB) k_upsert_p2md_rounds<F, MB><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, \
-                                                   a.uop >> 4, a.status, a.conc_erase, a.gated)
+#define WS_UR(F, MB, PH) k_upsert_p2md_rounds<F, MB, PH><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, \
+                                                   a.n, a.uop >> 4, a.status, a.conc_erase, a.gated)
     const bool f64 = a.d.tune_upsert == 3;
-    switch (a.d.tune_occ) {
-      case 5: if (f64) WS_UR(true, 5); else WS_UR(false, 5); break;
-      case 6: if (f64) WS_UR(true, 6); else WS_UR(false, 6); break;
-      default: if (f64) WS_UR(true, 1); else WS_UR(false, 1); break;
+    if (a.d.phased) {
+      if (f64) WS_UR(true, 1, true); else WS_UR(false, 1, true);
+    } else {
+      switch (a.d.tune_occ) {
+        case 5: if (f64) WS_UR(true, 5, false); else WS_UR(false, 5, false); break;
+        case 6: if (f64) WS_UR(true, 6, false); else WS_UR(false, 6, false); break;
+        default: if (f64) WS_UR(true, 1, false); else WS_UR(false, 1, false); break;
+      }
     }
 #undef WS_UR
     return;

@@ -496,7 +496,11 @@ __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64*
   }
 }
 
-template <bool F64, int MINB>
+// PHASED: the reference's bulk-synchronous mode (mode="phased",
+// sync.py:70-102): bucket locks are no-ops, so there is no try-lock, fence
+// or release, and publication falls back to a 128-bit CAS (foreign writers
+// race for free slots); a lost CAS retries the op next round.
+template <bool F64, int MINB, bool PHASED>
 __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, int merge,
                                                             u8* status, int conc_erase, int gated) {
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
     unsigned backoff = 64;
     while (__any_sync(0xFFFFFFFFu, pending)) {
       // phase 1: try-lock the primary (never blocks)
-      const bool hold0 = pending && try_lock_bucket(d.locks, b0);
+      const bool hold0 = pending && (PHASED || try_lock_bucket(d.locks, b0));
       // phase 2: primary tag blocks, one request per op
       u32 M0, Z0;
       coop_masks<false, F64>(d, hold0, b0, tag, M0, Z0);
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
           const int zc0 = __popc(Z0);
           used0 = 32 - (zc0 < d.zcc ? zc0 : d.zcc);
           if ((te || used0 >= d.shortcut) && b1 != b0) {
-            hold1 = try_lock_bucket(d.locks, b1);
+            hold1 = PHASED || try_lock_bucket(d.locks, b1);
             need1 = hold1;  // a failed try-lock retries the whole op next round
           } else {
             decided = true;  // shortcut (or b1 == b0): the primary it is
@@ -572,20 +576,31 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
       if (decided) {
         if (!Zt) {
           st = S_FULL;
+          pending = false;
         } else {
           const u64 slot = target * 32 + (__ffs(Zt) - 1);
           if (conc_erase) fence_acq_rel();
-          st_cell(d.cells + 2 * slot, key, val);
-          st_tag(d.tags + slot, tag);
-          st = S_INSERTED;
+          if (PHASED) {
+            if (publish_cell(d.cells + 2 * slot, key, val)) {
+              st_tag(d.tags + slot, tag);
+              st = S_INSERTED;
+              pending = false;
+            }
+          } else {
+            st_cell(d.cells + 2 * slot, key, val);
+            st_tag(d.tags + slot, tag);
+            st = S_INSERTED;
+            pending = false;
+          }
         }
-        pending = false;
       }
       // phase 4: one MEMBAR for the warp, then relaxed releases
-      __syncwarp();
-      fence_acq_rel();
-      if (hold1) red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
-      if (hold0) red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+      if (!PHASED) {
+        __syncwarp();
+        fence_acq_rel();
+        if (hold1) red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
+        if (hold0) red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+      }
       if (pending) {
         __nanosleep(backoff + 8 * (threadIdx.x & 31));
         if (backoff < 4096) backoff <<= 1;

@@ -66,3 +66,11 @@ for occ in (0, 8):
     t.tune(query_ilp=5, l2_policy=2, occupancy=occ)
     ms, (f, v) = timed(lambda: t.query_batch(q, check=False))
     print(f"query coop occ={occ}: {ms:.2f} ms ({n / ms / 1e6:.2f} G/s) hits={int(f.sum())}", flush=True)
+# phased (BSP) mode: no locks (reference sync.py:70-102)
+tp = make_table(TableConfig(design="p2_md", capacity_slots=slots, seed=42, mode="phased"))
+for rep in range(3):
+    tp.clear()
+    ms, st = timed(lambda: tp.upsert_batch(keys.view(torch.uint64), vals.view(torch.uint64), check=False), 1)
+    print(f"phased insert: {ms:.2f} ms ({n / ms / 1e6:.2f} G/s) bad={int((st != 0).sum())}", flush=True)
+ms, (f, v) = timed(lambda: tp.query_batch(q, check=False))
+print(f"phased query: {ms:.2f} ms ({n / ms / 1e6:.2f} G/s) hits={int(f.sum())}", flush=True)
