@@ -153,6 +153,13 @@ WS_API int ws_info(ws_table *t, ws_info_t *info);
 #define WS_TUNE_UPSERT 3    /* P2-MD upsert: 0 one thread per op, 1 lane-pair tiles,
                                2 warp-synchronous lock rounds, 3 rounds + 64-byte L2 fills (default) */
 #define WS_TUNE_OCCUPANCY 4 /* tuned kernels: request >= value CTAs/SM from ptxas (0 = compiler choice) */
+/* race-window widening for the adversarial duplicate-key test (reference
+ * bench/adversarial.py:40-93 DelayProfile): at the hook stages pre_reserve,
+ * pre_publish, pre_tombstone, pre_scan the generic kernels sleep up to
+ * DELAY_NS with probability DELAY_P16/65536.  Off (0) by default. */
+#define WS_TUNE_DELAY_NS 5
+#define WS_TUNE_DELAY_P16 6
+#define WS_TUNE_DELAY_SEED 7
 WS_API int ws_tune(ws_table *t, int knob, int value);
 
 /* hash-sharded multi-GPU routing (device pointers): split a batch into

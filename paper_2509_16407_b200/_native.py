@@ -34,6 +34,9 @@ WS_TUNE_QUERY_ILP = 1
 WS_TUNE_L2_POLICY = 2
 WS_TUNE_UPSERT = 3
 WS_TUNE_OCCUPANCY = 4
+WS_TUNE_DELAY_NS = 5
+WS_TUNE_DELAY_P16 = 6
+WS_TUNE_DELAY_SEED = 7
 
 
 class WsConfig(C.Structure):

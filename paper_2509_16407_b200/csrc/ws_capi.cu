@@ -779,6 +779,17 @@ int ws_tune(ws_table* t, int knob, int value) {
     case WS_TUNE_OCCUPANCY:
       t->d.tune_occ = value;
       return WS_OK;
+    case WS_TUNE_DELAY_NS:
+      if (value < 0) return WS_ERR_ARG;
+      t->d.delay_ns = (u32)value;
+      return WS_OK;
+    case WS_TUNE_DELAY_P16:
+      if (value < 0 || value > 65536) return WS_ERR_ARG;
+      t->d.delay_p16 = (u32)value;
+      return WS_OK;
+    case WS_TUNE_DELAY_SEED:
+      t->d.delay_seed = mix64((u64)(unsigned)value);
+      return WS_OK;
     case WS_TUNE_UPSERT:
       if (value < 0 || value > 3) return WS_ERR_ARG;
       t->d.tune_upsert = value;

@@ -45,6 +45,11 @@ struct Dev {
   int tune_l2pol;  // 1: tag loads evict_last, cell loads evict_first
   int tune_upsert; // P2-MD upsert kernel: 0 generic one-thread-per-op, 1 lane pair, 2/3 rounds
   int tune_occ;    // minimum resident CTAs per SM requested from ptxas (register cap)
+  // delay injection at the reference's scheduling-hook stages
+  // (tables/base.py:66-69, bench/adversarial.py:40-93): with probability
+  // delay_p16/65536 a stage sleeps up to delay_ns; 0 = off (generic kernels)
+  u32 delay_ns, delay_p16;
+  u64 delay_seed;
 };
 
 __device__ __forceinline__ u64 apply_merge(int m, u64 old, u64 nv) {
@@ -118,6 +123,13 @@ struct Ctx {
     return false;
   }
   __device__ __forceinline__ void ldc(u64 i, u64& k, u64& v) { load_cell<RO>(cell(i), k, v); }
+  enum Stage { PRE_RESERVE = 1, PRE_PUBLISH = 2, PRE_TOMBSTONE = 3, PRE_SCAN = 4 };
+  __device__ __forceinline__ void hook(int stage, u64 key) {
+    if (RO || INSTR || !d.delay_ns) return;
+    const u64 r = mix64(d.delay_seed ^ (key * 0x9E3779B97F4A7C15ull) ^ ((u64)stage << 56) ^
+                        ((u64)(blockIdx.x * blockDim.x + threadIdx.x) << 20) ^ clock64());
+    if ((u32)(r & 0xFFFF) < d.delay_p16) __nanosleep((u32)((r >> 32) % d.delay_ns));
+  }
   __device__ __forceinline__ u16 ldt(u64 i) { return RO ? ld_tag_ro(d.tags + i) : ld_tag(d.tags + i); }
   __device__ __forceinline__ u64 hb(int i, u64 key, const Mod& m) const {
     return m(mix64(key ^ d.seeds[i]) >> 16);
@@ -302,6 +314,7 @@ struct Ctx {
       if constexpr (!MD) {
         if (hint < 0) hint = find_free(lo, n);
         if (hint < 0) return -1;
+        hook(PRE_PUBLISH, key);
         st_cell(cell((u64)hint), key, val);
         touch(16 * (u64)hint);
         return hint;
@@ -311,6 +324,7 @@ struct Ctx {
         touch(16 * (u64)z);
         // a zero tag may be a slot an eraser just tombstoned: order its
         // tombstone store (released by the eraser's fence) before ours
+        hook(PRE_PUBLISH, key);
         if (conc_erase) fence_acq_rel();
         st_cell(cell((u64)z), key, val);
         st_tag(d.tags + z, tag);
@@ -323,6 +337,7 @@ struct Ctx {
         if (hint < 0) hint = find_free(lo, n);
         if (hint < 0) return -1;
         touch(16 * (u64)hint);
+        hook(PRE_RESERVE, key);
         if (publish_cell(cell((u64)hint), key, val)) break;
         hint = -1;
       }
@@ -336,6 +351,7 @@ struct Ctx {
         if (z < 0) return -1;
       }
       touch(16 * (u64)z);
+      hook(PRE_RESERVE, key);
       if (publish_cell(cell((u64)z), key, val)) break;
       z = md_first_zero(lo, hi, (u64)z + 1);
     }
@@ -357,6 +373,7 @@ struct Ctx {
 
   // reference openaddr.py:187-197: flag, tombstone, then clear the tag
   __device__ void tombstone(u64 idx) {
+    hook(PRE_TOMBSTONE, idx);
     if (ld_u32_relaxed(d.state) == 0) st_u32_relaxed(d.state, 1u);
     fence_acq_rel();
     st_cell(cell(idx), TOMB, 0);
@@ -507,6 +524,7 @@ struct Ctx {
     const u64 b0 = hb(0, key, d.nbm);
     const bool locked = !d.lock_elided;
     if (locked) lock(b0);
+    hook(PRE_SCAN, key);
     u64 v;
     const i64 idx = p2_find(key, v, true);
     if (idx >= 0) tombstone((u64)idx);

@@ -573,6 +573,13 @@ class HashTable:
         if l2_policy is not None:
             self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_L2_POLICY, int(l2_policy)))
 
+    def set_delays(self, max_ns=0, prob=0.0, seed=0):
+        """Device delay injection at the reference's hook stages (race-window
+        widening for adversarial tests; generic kernels only)."""
+        self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_DELAY_NS, int(max_ns)))
+        self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_DELAY_P16, int(round(prob * 65536))))
+        self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_DELAY_SEED, int(seed) & 0x7FFFFFFF))
+
     def clear(self):
         """Back to the freshly constructed state without reallocating
         (stream-ordered on the current CUDA stream)."""

@@ -1,0 +1,52 @@
+"""Device adversarial duplicate-key race (paper §4.1; reference
+tests/test_bench.py:153-169): safe designs never commit a key twice, the
+lock-elided unsafe reference does, and a serial replay never does."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+SAFE = ["double", "double_md", "p2", "p2_md", "iceberg", "iceberg_md", "cuckoo", "chaining"]
+
+
+@pytest.mark.parametrize("design", SAFE)
+def test_safe_designs_zero_duplicates_heavy_delays(design):
+    from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
+    rep = run_adversarial(design, buckets=4000, trials=3, seed=5, profile=DelayProfile(0.35, 20_000))
+    assert rep["duplicate_buckets"] == 0, rep
+
+
+def test_safe_p2md_large_no_delay():
+    from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
+    rep = run_adversarial("p2_md", buckets=200_000, trials=5, seed=11, profile=DelayProfile.off())
+    assert rep["duplicate_buckets"] == 0, rep
+
+
+def test_unsafe_reference_races():
+    from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
+    rep = run_adversarial("unsafe_reference", buckets=20_000, trials=3, seed=5,
+                          profile=DelayProfile(0.35, 20_000))
+    assert rep["duplicate_buckets"] >= 1, rep
+
+
+def test_serial_replay_never_races():
+    """The same three-actor script replayed in index order on one device
+    thread (reference single_thread=True) gives zero duplicates even for the
+    unsafe design."""
+    from paper_2509_16407_b200 import make_table
+    from paper_2509_16407_b200.adversarial import config_for_primary_buckets, generate_pairs
+    cfg = config_for_primary_buckets("unsafe_reference", 3000, 5)
+    t = make_table(cfg)
+    xs, ys = generate_pairs(t, 3000, 5)
+    t.upsert_batch(xs, np.ones(3000, np.uint64))
+    ops, keys, vals = [], [], []
+    for b in range(3000):  # the reference's per-bucket actor order
+        ops += [1, 0 | (1 << 4), 0 | (1 << 4)]
+        keys += [xs[b], ys[b], ys[b]]
+        vals += [0, 1, 2]
+    st, _ = t.mixed_batch(np.array(ops, np.uint8), np.array(keys, np.uint64), np.array(vals, np.uint64),
+                          serial=True)
+    assert t.duplicate_scan() == {}
+    assert dict(t.items()) == {int(y): 1 for y in ys}
