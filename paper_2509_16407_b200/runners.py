@@ -1,0 +1,271 @@
+"""Device workload runners for the BASELINE.json configs (the GPU counterparts
+of reference bench/runners.py).  Every runner verifies results, times the
+device batches with CUDA events, and returns a report dict plus reference-
+schema CSV rows (instrument.Row).
+
+* ``run_config1``  double hashing 2^20: insert to 0.85, 2^19 interleaved
+  50/50 queries (reference runners.py:130-144, 172-181)
+* ``run_load_sweep``  insert / query / probes per load point, then an erase
+  drain (reference runners.py:172-256); config 4 = cuckoo / chaining sweeps
+* ``run_aging``  prefill 0.85, then mixed batches: Zipf upsert-ADD on live
+  keys + fresh inserts, erase of the oldest slice, queries on untouched live
+  keys and on absent keys (reference runners.py:259-353; config 3)
+* ``run_kmer``  canonical 31-mer counting with upsert-ADD (config 5 on one
+  table / shard)
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .core import TableConfig
+from .instrument import Row
+from .workload import derive_seed, gen_uniform_keys, kmer_keys, mix64_np, zipf_ranks
+
+U64 = np.uint64
+LOAD_POINTS = tuple(round(0.05 * i, 2) for i in range(1, 19))
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev(a, device):
+    torch = _torch()
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint8:
+        return torch.from_numpy(a).to(device)
+    return torch.from_numpy(a.astype(U64, copy=False).view(np.int64)).to(device).view(torch.uint64)
+
+
+def _np(t):
+    torch = _torch()
+    t = t.cpu()
+    if t.dtype == torch.uint64:
+        return t.view(torch.int64).numpy().view(U64)
+    return t.numpy()
+
+
+class _Timer:
+    def __init__(self):
+        torch = _torch()
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.b = torch.cuda.Event(enable_timing=True)
+
+    def __enter__(self):
+        self.a.record()
+        return self
+
+    def __exit__(self, *exc):
+        self.b.record()
+        self.b.synchronize()
+        self.ms = self.a.elapsed_time(self.b)
+
+
+def _mops(n, ms):
+    return n / ms / 1e3 if ms > 0 else 0.0
+
+
+def run_config1(seed: int = 42, capacity: int = 1 << 20, design: str = "double") -> dict:
+    from .tables import make_table
+    t = make_table(TableConfig(design=design, capacity_slots=capacity, seed=seed))
+    dev = t.device
+    n = int(capacity * 0.85)
+    keys = gen_uniform_keys(seed, n)
+    nq = 1 << 19
+    miss = gen_uniform_keys(derive_seed(seed, 0xFEED), nq // 2)
+    hits = keys[: nq // 2]
+    q = np.empty(nq, dtype=U64)
+    q[0::2], q[1::2] = hits, miss
+    dk, dv, dq = _dev(keys, dev), _dev(keys & U64(0xFFFF), dev), _dev(q, dev)
+    t.upsert_batch(dk, dv)  # warm the kernels
+    t.clear()
+    with _Timer() as ti:
+        st = t.upsert_batch(dk, dv, check=False)
+    with _Timer() as tq:
+        found, vals = t.query_batch(dq, check=False)
+    f, v = _np(found).astype(bool), _np(vals)
+    ok = (_np(st) == 0).all() and f[0::2].all() and not f[1::2].any() and \
+        (v[0::2] == (hits & U64(0xFFFF))).all()
+    rows = [Row(design, "concurrent", capacity, 128, "throughput", "insert", 0.85, 0, n, ti.ms / 1e3,
+                _mops(n, ti.ms)),
+            Row(design, "concurrent", capacity, 128, "throughput", "query_5050", 0.85, 0, nq, tq.ms / 1e3,
+                _mops(nq, tq.ms))]
+    return {"ok": bool(ok), "insert_mops": _mops(n, ti.ms), "query_mops": _mops(nq, tq.ms), "rows": rows}
+
+
+def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_POINTS,
+                   query_sample: int = 1 << 20, probe_sample: int = 4096, mode: str = "concurrent",
+                   drain: bool = True) -> dict:
+    """Insert to each load point (timed batch), 50/50 queries (timed), probe
+    means from instrumented batches (reference ProbeRecorder semantics), then
+    an erase drain in 18 slices."""
+    from .tables import OP_QUERY, OP_UPSERT, make_table
+    cfg = TableConfig(design=design, capacity_slots=capacity, seed=seed, mode=mode)
+    t = make_table(cfg)
+    dev = t.device
+    cap = t.capacity_slots
+    n_max = int(cap * load_points[-1])
+    keys = gen_uniform_keys(seed, n_max)
+    neg = gen_uniform_keys(derive_seed(seed, 0xFEED), query_sample)
+    rows, points, fulls = [], [], 0
+    placed = 0
+    for point in load_points:
+        target = int(cap * point)
+        batch = keys[placed:target]
+        # the batch's last probe_sample inserts run instrumented
+        np_ins = min(probe_sample, len(batch) // 4)
+        timed = batch[: len(batch) - np_ins]
+        with _Timer() as ti:
+            st = t.upsert_batch(_dev(timed, dev), _dev(timed, dev), check=False)
+        fulls += int((_np(st) == 2).sum())
+        ins_probe = 0.0
+        if np_ins:
+            pst, _v, pr, _l = t.probe_batch(np.full(np_ins, OP_UPSERT, np.uint8), batch[-np_ins:],
+                                            batch[-np_ins:], serial=False)
+            fulls += int((pst == 2).sum())
+            ins_probe = float(pr.mean())
+        placed = target
+        qn = min(query_sample, placed)
+        pos = keys[:placed][np.linspace(0, placed - 1, qn // 2).astype(np.int64)]
+        q = np.concatenate([pos, neg[: qn - len(pos)]])
+        with _Timer() as tq:
+            found, _vals = t.query_batch(_dev(q, dev), check=False)
+        f = _np(found).astype(bool)
+        ok = bool(f[: len(pos)].all() and not f[len(pos):].any())
+        ps = min(probe_sample, len(pos))
+        _s, _v, prp, _l = t.probe_batch(np.full(ps, OP_QUERY, np.uint8), pos[:ps], serial=False)
+        _s, _v, prn, _l = t.probe_batch(np.full(ps, OP_QUERY, np.uint8), neg[:ps], serial=False)
+        rows += [
+            Row(design, mode, cap, 128, "throughput", "insert", point, 0, len(timed), ti.ms / 1e3,
+                _mops(len(timed), ti.ms)),
+            Row(design, mode, cap, 128, "probe", "insert", point, 0, np_ins, 0, 0, ins_probe),
+            Row(design, mode, cap, 128, "throughput", "query_5050", point, 0, qn, tq.ms / 1e3, _mops(qn, tq.ms)),
+            Row(design, mode, cap, 128, "probe", "query_pos", point, 0, ps, 0, 0, float(prp.mean())),
+            Row(design, mode, cap, 128, "probe", "query_neg", point, 0, ps, 0, 0, float(prn.mean())),
+        ]
+        points.append({"load": point, "insert_mops": _mops(len(timed), ti.ms), "query_mops": _mops(qn, tq.ms),
+                       "probes_insert": ins_probe, "probes_query_pos": float(prp.mean()),
+                       "probes_query_neg": float(prn.mean()), "queries_ok": ok, "fulls_so_far": fulls})
+    if drain:
+        live = keys[:placed]
+        chunk = -(-len(live) // 18)
+        for off in range(0, len(live), chunk):
+            sl = live[off:off + chunk]
+            with _Timer() as te:
+                gone = t.erase_batch(_dev(sl, dev), check=False)
+            rows.append(Row(design, mode, cap, 128, "throughput", "erase", round((len(live) - off) / cap, 4), 0,
+                            len(sl), te.ms / 1e3, _mops(len(sl), te.ms)))
+            if not bool(_np(gone).all()):
+                points.append({"drain_error": off})
+        points.append({"after_drain_occupied": t.occupied_count()})
+    return {"design": design, "capacity": cap, "fulls": fulls, "points": points, "rows": rows}
+
+
+def run_aging(design: str = "iceberg_md", capacity: int = 1 << 26, iterations: int = 20,
+              slice_fraction: float = 0.01, seed: int = 42, theta: float = 0.99,
+              zipf_ops_per_slice: float = 1.0) -> dict:
+    """Aging with Zipf upsert-ADD (config 3).  Per iteration one mixed launch:
+    fresh keys inserted (ADD), a Zipf(theta) sample of live keys upsert-ADDed,
+    the oldest slice erased, the next slice queried (present) and absent keys
+    queried -- key roles disjoint, so results are order-independent.  Every
+    status / found flag / value is checked against a numpy model; the final
+    table checksum is compared to the model's."""
+    from .tables import OP_ERASE, OP_QUERY, OP_UPSERT, make_table
+    torch = _torch()
+    t = make_table(TableConfig(design=design, capacity_slots=capacity, seed=seed))
+    dev = t.device
+    cap = t.capacity_slots
+    fill = int(cap * 0.85)
+    sl = max(8, int(fill * slice_fraction))
+    stream = gen_uniform_keys(seed, fill + sl * iterations)
+    absent = gen_uniform_keys(derive_seed(seed, 0xADAE), sl * iterations)
+    values = np.zeros(len(stream), dtype=U64)  # model: value of stream[i] while live
+    values[:fill] = stream[:fill] & U64(0xFFFF)
+    st = t.upsert_batch(_dev(stream[:fill], dev), _dev(values[:fill], dev))
+    if int((_np(st) != 0).sum()):
+        raise RuntimeError("aging prefill did not insert every key")
+    head, tail = 0, fill
+    ADD = OP_UPSERT | (2 << 4)
+    rows, its = [], []
+    total_ok = True
+    for it in range(iterations):
+        new = np.arange(tail, tail + sl)
+        old = np.arange(head, head + sl)
+        pos = np.arange(head + sl, head + 2 * sl)
+        live_lo = head + 2 * sl  # Zipf universe: live keys outside the erase / query slices
+        uni = tail - live_lo
+        nz = int(sl * zipf_ops_per_slice)
+        zr = zipf_ranks(uni, nz, theta, seed=derive_seed(seed, it)) - 1
+        zidx = live_lo + zr
+        zval = (mix64_np(np.arange(nz, dtype=U64) + U64(it)) & U64(0xFF))
+        ops = np.concatenate([np.full(sl, ADD), np.full(nz, ADD), np.full(sl, OP_ERASE),
+                              np.full(sl, OP_QUERY), np.full(sl, OP_QUERY)]).astype(np.uint8)
+        keys = np.concatenate([stream[new], stream[zidx], stream[old], stream[pos],
+                               absent[it * sl:(it + 1) * sl]])
+        newv = stream[new] & U64(0xFFFF)
+        vals = np.concatenate([newv, zval, np.zeros(3 * sl, U64)])
+        perm = np.argsort((keys * U64(0x9E3779B97F4A7C15)) & U64(0xFFFFFFFF), kind="stable")
+        with _Timer() as tm:
+            s, v = t.mixed_batch(_dev(ops[perm], dev), _dev(keys[perm], dev), _dev(vals[perm], dev),
+                                 check=False)
+        s, v = _np(s), _np(v)
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(len(perm))
+        s, v = s[inv], v[inv]
+        # model: statuses and values
+        o = 0
+        ok = (s[o:o + sl] == 0).all()  # fresh inserts
+        o += sl
+        ok &= (s[o:o + nz] == 1).all()  # Zipf adds hit live keys
+        o += nz
+        ok &= (s[o:o + sl] == 1).all()  # erases found
+        o += sl
+        ok &= (s[o:o + sl] == 1).all() and (v[o:o + sl] == values[pos]).all()  # present, pre-add values
+        o += sl
+        ok &= not s[o:o + sl].any()  # absent
+        with np.errstate(over="ignore"):
+            np.add.at(values, zidx, zval)
+        values[new] = newv
+        values[old] = 0
+        head += sl
+        tail += sl
+        total_ok &= bool(ok)
+        n_ops = len(ops)
+        its.append({"iteration": it, "ops": n_ops, "ms": tm.ms, "mops": _mops(n_ops, tm.ms), "ok": bool(ok)})
+        rows.append(Row(design, "concurrent", cap, 128, "throughput", "mixed", round(fill / cap, 4), 0, n_ops,
+                        tm.ms / 1e3, _mops(n_ops, tm.ms)))
+    live = np.arange(head, tail)
+    with np.errstate(over="ignore"):
+        lk, lv = stream[live], values[live]
+        want = (len(live), int(lk.sum(dtype=U64)), int(lv.sum(dtype=U64)),
+                int(np.bitwise_xor.reduce(mix64_np(lk ^ mix64_np(lv)))))
+    got = t.checksum()
+    del torch
+    return {"design": design, "capacity": cap, "slice": sl, "iterations": its, "ok": total_ok,
+            "checksum_ok": got == want, "duplicates": t.duplicate_count(),
+            "mean_mops": float(np.mean([i["mops"] for i in its])), "rows": rows}
+
+
+def run_kmer(genome_len: int = 1 << 24, k: int = 31, capacity: int = 1 << 25, design: str = "p2_md",
+             seed: int = 7, batches: int = 4) -> dict:
+    """Count canonical k-mers of a synthetic genome with upsert-ADD; every
+    count is checked against numpy's."""
+    from .tables import make_table
+    t = make_table(TableConfig(design=design, capacity_slots=capacity, seed=seed))
+    dev = t.device
+    km = kmer_keys(genome_len, k, seed)
+    ones = np.ones(len(km), dtype=U64)
+    ms = 0.0
+    for part in np.array_split(np.arange(len(km)), batches):
+        with _Timer() as tm:
+            st = t.upsert_batch(_dev(km[part], dev), _dev(ones[part], dev), merge="add", check=False)
+        ms += tm.ms
+        if int((_np(st) == 2).sum()):
+            raise RuntimeError("k-mer table hit FULL: raise capacity")
+    u, c = np.unique(km, return_counts=True)
+    found, vals = t.query_batch(_dev(u, dev))
+    ok = bool(_np(found).all() and (_np(vals) == c.astype(U64)).all())
+    return {"kmers": len(km), "distinct": len(u), "load": len(u) / t.capacity_slots, "ok": ok,
+            "ms": ms, "mops": _mops(len(km), ms), "occupied": t.occupied_count()}
