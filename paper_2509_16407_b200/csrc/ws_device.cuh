@@ -169,10 +169,10 @@ __device__ __forceinline__ void red_and_release(u32* p, u32 m) {
 __device__ __forceinline__ void lock_bucket(u32* locks, u64 b) {
   u32* w = locks + (b >> 5);
   const u32 bit = 1u << (b & 31);
-  unsigned ns = 32;
+  unsigned ns = 16;
   while (atom_or_acquire(w, bit) & bit) {
     __nanosleep(ns);
-    if (ns < 2048) ns <<= 1;
+    if (ns < 256) ns <<= 1;  // short cap: hot keys hand the lock over quickly
   }
 }
 __device__ __forceinline__ void unlock_bucket(u32* locks, u64 b) {

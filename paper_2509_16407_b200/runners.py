@@ -73,13 +73,14 @@ def run_config1(seed: int = 42, capacity: int = 1 << 20, design: str = "double")
     dev = t.device
     n = int(capacity * 0.85)
     keys = gen_uniform_keys(seed, n)
-    nq = 1 << 19
+    nq = min(1 << 19, 2 * (n // 2))
     miss = gen_uniform_keys(derive_seed(seed, 0xFEED), nq // 2)
     hits = keys[: nq // 2]
     q = np.empty(nq, dtype=U64)
     q[0::2], q[1::2] = hits, miss
     dk, dv, dq = _dev(keys, dev), _dev(keys & U64(0xFFFF), dev), _dev(q, dev)
-    t.upsert_batch(dk, dv)  # warm the kernels
+    t.upsert_batch(dk, dv)  # warm the kernels (lazy module loading) outside the timed region
+    t.query_batch(dq)
     t.clear()
     with _Timer() as ti:
         st = t.upsert_batch(dk, dv, check=False)
