@@ -25,6 +25,7 @@ WS_ERR_INVALID_OP = -6
 WS_F_SYNC_CHECK = 1
 WS_F_NO_CHECK = 2
 WS_F_SERIAL = 4
+WS_F_COMBINE = 8
 
 EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_erase", "ws_mixed",
            "ws_locate", "ws_probe_counts", "ws_occupied", "ws_export_items",

@@ -216,9 +216,9 @@ int chain_grow(ws_table* t, cudaStream_t s) {
 }
 
 // Run one batch whose buffers are all device-resident.
-int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
-               u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
-               bool query_only) {
+int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
+                     u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
+                     bool query_only) {
   const bool sync = (flags & WS_F_SYNC_CHECK) != 0;
   int rc = validate(t, keys, ops, n, s, sync, flags);
   if (rc) return rc;
@@ -254,6 +254,129 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   return rc;
 }
 
+// ------------------------------------------------------------------ combining
+// WS_F_COMBINE: same-key upserts of one batch are reduced before they touch
+// the table (radix sort by key, runs of equal (key, op byte) folded with the
+// op's merge), one op per run is applied, and statuses are expanded: the run
+// leader gets the real status, other members UPDATED (FULL if the leader was).
+// Equivalent to some serial order of the batch for every merge; the point is
+// Zipf hot keys, whose ops would otherwise serialise on one bucket lock.
+struct OpVal {
+  u64 v;
+  u32 op;
+  u32 pad;
+};
+struct CombineOp {
+  __device__ __forceinline__ OpVal operator()(const OpVal& a, const OpVal& b) const {
+    const int m = a.op >> 4;
+    OpVal r = a;
+    r.v = m == M_KEEP ? a.v : apply_merge(m, a.v, b.v);
+    return r;
+  }
+};
+
+__device__ __forceinline__ u8 op_at(const u8* ops, u8 uop, u64 i) { return ops ? ops[i] : uop; }
+
+__global__ void k_comb_iota(u64 n, u32* idx) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) idx[i] = (u32)i;
+}
+
+__global__ void k_comb_heads(const u64* sk, const u32* si, const u8* ops, u8 uop, const u64* vals, u64 n,
+                             u32* head, OpVal* ov) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
+    const u8 op = op_at(ops, uop, si[j]);
+    bool h = j == 0 || (op & 15) != OP_UPSERT;
+    if (!h) h = sk[j] != sk[j - 1] || op_at(ops, uop, si[j - 1]) != op;
+    head[j] = h;
+    ov[j] = OpVal{vals ? vals[si[j]] : 0ull, op, 0};
+  }
+}
+
+__global__ void k_comb_groups(const u64* sk, const u32* si, const u32* head, const u32* seg, const u8* ops, u8 uop,
+                              u64 n, u64* gkey, u8* gop) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
+    if (!head[j]) continue;
+    const u32 g = seg[j] - 1;
+    gkey[g] = sk[j];
+    gop[g] = op_at(ops, uop, si[j]);
+  }
+}
+
+__global__ void k_comb_vals(const OpVal* agg, u64 ng, u64* gval) {
+  for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < ng; g += (u64)gridDim.x * blockDim.x)
+    gval[g] = agg[g].v;
+}
+
+__global__ void k_comb_expand(const u32* si, const u32* head, const u32* seg, u64 n, const u8* gst, const u64* gvo,
+                              u8* status, u64* vout) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
+    const u32 g = seg[j] - 1;
+    const u32 i = si[j];
+    const u8 gs = gst[g];
+    if (status) status[i] = head[j] ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
+    if (vout) vout[i] = head[j] ? gvo[g] : 0ull;
+  }
+}
+
+int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
+               u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
+               bool query_only) {
+  if (!(flags & WS_F_COMBINE) || query_only || !has_upsert || n < 2 || n >= (1ull << 32) ||
+      (flags & WS_F_SERIAL))
+    return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s, flags & ~WS_F_COMBINE, has_erase,
+                            has_upsert, query_only);
+  int rc = validate(t, keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags);
+  if (rc) return rc;
+  // scratch: sorted keys / indices, heads, segment ids, op-values, groups
+  u64 *sk = nullptr, *gkey = nullptr, *gval = nullptr, *gvo = nullptr;
+  u32 *idx = nullptr, *si = nullptr, *head = nullptr, *seg = nullptr, *uniq = nullptr;
+  OpVal *ov = nullptr, *agg = nullptr;
+  u8 *gop = nullptr, *gst = nullptr;
+  u64* nruns = nullptr;
+  WS_CK(cudaMallocAsync((void**)&sk, 8 * n, s));
+  WS_CK(cudaMallocAsync((void**)&idx, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&si, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&head, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&seg, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&uniq, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&ov, sizeof(OpVal) * n, s));
+  WS_CK(cudaMallocAsync((void**)&agg, sizeof(OpVal) * n, s));
+  WS_CK(cudaMallocAsync((void**)&nruns, 8, s));
+  k_comb_iota<<<grid_for(n), kThreads, 0, s>>>(n, idx);
+  size_t tb = 0, tb2 = 0, tb3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
+  cub::DeviceScan::InclusiveSum(nullptr, tb2, head, seg, (int64_t)n, s);
+  cub::DeviceReduce::ReduceByKey(nullptr, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
+  void* tmp = nullptr;
+  const size_t tmax = std::max(tb, std::max(tb2, tb3)) + 16;
+  WS_CK(cudaMallocAsync(&tmp, tmax, s));
+  cub::DeviceRadixSort::SortPairs(tmp, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
+  k_comb_heads<<<grid_for(n), kThreads, 0, s>>>(sk, si, ops, uop, vals, n, head, ov);
+  cub::DeviceScan::InclusiveSum(tmp, tb2, head, seg, (int64_t)n, s);
+  cub::DeviceReduce::ReduceByKey(tmp, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
+  WS_CK(cudaMemcpyAsync(t->h_pin, nruns, 8, cudaMemcpyDeviceToHost, s));
+  WS_CK(cudaStreamSynchronize(s));
+  const u64 ng = t->h_pin[0];
+  WS_CK(cudaMallocAsync((void**)&gkey, 8 * ng, s));
+  WS_CK(cudaMallocAsync((void**)&gval, 8 * ng, s));
+  WS_CK(cudaMallocAsync((void**)&gvo, 8 * ng, s));
+  WS_CK(cudaMallocAsync((void**)&gop, ng, s));
+  WS_CK(cudaMallocAsync((void**)&gst, ng, s));
+  k_comb_groups<<<grid_for(n), kThreads, 0, s>>>(sk, si, head, seg, ops, uop, n, gkey, gop);
+  k_comb_vals<<<grid_for(ng), kThreads, 0, s>>>(agg, ng, gval);
+  WS_CK(cudaGetLastError());
+  rc = run_device_plain(t, ops ? gop : nullptr, uop, gkey, vals ? gval : nullptr, ng, gst, gvo, s,
+                        (flags & ~(WS_F_COMBINE | WS_F_SYNC_CHECK)) | WS_F_NO_CHECK, has_erase, has_upsert, false);
+  if (!rc) {
+    k_comb_expand<<<grid_for(n), kThreads, 0, s>>>(si, head, seg, n, gst, gvo, status, vout);
+    rc = cuda_err(cudaGetLastError());
+  }
+  for (void* p : {(void*)sk, (void*)idx, (void*)si, (void*)head, (void*)seg, (void*)uniq, (void*)ov, (void*)agg,
+                  (void*)nruns, tmp, (void*)gkey, (void*)gval, (void*)gvo, (void*)gop, (void*)gst})
+    cudaFreeAsync(p, s);
+  return rc;
+}
+
 // Host-buffer batches: staged through device memory in 4M-op chunks on three
 // streams -- H2D on s_in, validation + kernels on the caller's stream, D2H on
 // s_aux -- so copies in both directions overlap compute.  Queries never
@@ -286,7 +409,7 @@ int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   WS_CK(cudaStreamWaitEvent(t->s_aux, t->ev_b, 0));
   const bool chain_up = t->cfg.design == D_CHAINING && has_upsert;
   const u64 chunk = chain_up ? n : (u64)1 << 22;
-  const u32 sub = WS_F_NO_CHECK | (flags & WS_F_SERIAL);
+  const u32 sub = WS_F_NO_CHECK | (flags & (WS_F_SERIAL | WS_F_COMBINE));
   int rc = WS_OK;
   auto h2d = [&](u64 off, u64 m) -> int {
     if (hk) WS_CK(cudaMemcpyAsync((void*)(dk + off), keys + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));

@@ -166,7 +166,7 @@ def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_
 
 def run_aging(design: str = "iceberg_md", capacity: int = 1 << 26, iterations: int = 20,
               slice_fraction: float = 0.01, seed: int = 42, theta: float = 0.99,
-              zipf_ops_per_slice: float = 1.0) -> dict:
+              zipf_ops_per_slice: float = 1.0, combine: bool = True) -> dict:
     """Aging with Zipf upsert-ADD (config 3).  Per iteration one mixed launch:
     fresh keys inserted (ADD), a Zipf(theta) sample of live keys upsert-ADDed,
     the oldest slice erased, the next slice queried (present) and absent keys
@@ -210,7 +210,7 @@ def run_aging(design: str = "iceberg_md", capacity: int = 1 << 26, iterations: i
         perm = np.argsort((keys * U64(0x9E3779B97F4A7C15)) & U64(0xFFFFFFFF), kind="stable")
         with _Timer() as tm:
             s, v = t.mixed_batch(_dev(ops[perm], dev), _dev(keys[perm], dev), _dev(vals[perm], dev),
-                                 check=False)
+                                 check=False, combine=combine)
         s, v = _np(s), _np(v)
         inv = np.empty_like(perm)
         inv[perm] = np.arange(len(perm))

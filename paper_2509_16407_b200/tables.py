@@ -401,7 +401,7 @@ class HashTable:
         # true async DMA (torch caches pinned blocks across calls)
         return torch.empty(n, dtype=dtype, pin_memory=n >= (1 << 20))
 
-    def upsert_batch(self, keys, values, merge=None, check=True, out=None):
+    def upsert_batch(self, keys, values, merge=None, check=True, out=None, combine=False):
         """Concurrent upsert of a batch; returns a uint8 status tensor
         (0 INSERTED, 1 UPDATED, 2 FULL) on the keys' device (or `out`)."""
         torch = _torch()
@@ -412,6 +412,8 @@ class HashTable:
         st = self._out(kc, len(k), torch.uint8, torch) if out is None else _checked_out(out, len(k), torch.uint8)
         self._dirty()
         fl = _native.WS_F_SYNC_CHECK if check else _native.WS_F_NO_CHECK
+        if combine:
+            fl |= _native.WS_F_COMBINE
         self._check(self._lib.ws_upsert(self._h, kp, vp, len(k), merge_id(merge), st.data_ptr(),
                                         self._stream(), fl))
         return st
@@ -441,7 +443,7 @@ class HashTable:
         self._check(self._lib.ws_erase(self._h, kp, len(k), found.data_ptr(), self._stream(), fl))
         return found.bool()
 
-    def mixed_batch(self, ops, keys, values=None, check=True, serial=False):
+    def mixed_batch(self, ops, keys, values=None, check=True, serial=False, combine=False):
         """One launch of mixed ops (byte = kind | merge << 4, kind 0 upsert /
         1 erase / 2 query).  Returns (status uint8, values uint64): upsert
         status, erase/query found flag, query value."""
@@ -457,6 +459,8 @@ class HashTable:
         fl = _native.WS_F_SYNC_CHECK if check else _native.WS_F_NO_CHECK
         if serial:
             fl |= _native.WS_F_SERIAL
+        if combine:
+            fl |= _native.WS_F_COMBINE
         self._check(self._lib.ws_mixed(self._h, op, kp, vp, len(k), st.data_ptr(), vo.data_ptr(),
                                        self._stream(), fl))
         return st, vo

@@ -342,3 +342,31 @@ def test_sharded_table_single_rank_is_the_local_table():
     f, v = st.query_batch(_cuda(keys))
     assert bool(f.all())
     assert st.checksum()[0] == 50_000
+
+
+@pytest.mark.parametrize("merge", ["add", "max", "min", "keep", None])
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "chaining"])
+def test_combined_hot_key_batch_matches_oracle(design, merge):
+    """WS_F_COMBINE folds same-key upserts before applying them: the final
+    map equals the oracle's for commutative merges (and is one of the valid
+    serial outcomes for keep / replace), exactly one INSERTED per new key."""
+    from paper_2509_16407_b200.workload import zipf_ranks
+    cfg = cfg_for(design, 1 << 15 if design != "chaining" else 7 * 2048, seed=4)
+    t = _table(cfg)
+    uni = _keys(9, 5000)
+    keys = uni[zipf_ranks(5000, 100_000, 0.99, seed=1) - 1]
+    vals = (np.arange(len(keys), dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals), merge=merge, combine=True))
+    u, first, inv = np.unique(keys, return_index=True, return_inverse=True)
+    assert int((st == 0).sum()) == len(u) and int((st == 2).sum()) == 0
+    got = dict(t.items())
+    if merge in ("add", "max", "min"):
+        o = _oracle(cfg)
+        o.upsert_batch(keys, vals, merge)
+        assert got == o.as_dict()
+    else:  # keep / replace: each key holds one of its batch values
+        per = {}
+        for k, v in zip(keys.tolist(), vals.tolist()):
+            per.setdefault(k, set()).add(v)
+        assert set(got) == set(per) and all(got[k] in per[k] for k in got)
+    assert t.duplicate_scan() == {}
