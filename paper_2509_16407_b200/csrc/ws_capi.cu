@@ -914,7 +914,7 @@ int ws_tune(ws_table* t, int knob, int value) {
       t->d.delay_seed = mix64((u64)(unsigned)value);
       return WS_OK;
     case WS_TUNE_UPSERT:
-      if (value < 0 || value > 3) return WS_ERR_ARG;
+      if (value < 0 || value > 4) return WS_ERR_ARG;
       t->d.tune_upsert = value;
       return WS_OK;
     default: return WS_ERR_ARG;

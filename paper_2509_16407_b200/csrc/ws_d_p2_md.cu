@@ -41,8 +41,12 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
     g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
 #define WS_UR(F, MB, PH) k_upsert_p2md_rounds<F, MB, PH><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, \
                                                    a.n, a.uop >> 4, a.status, a.conc_erase, a.gated)
-    const bool f64 = a.d.tune_upsert == 3;
-    if (a.d.phased) {
+    const bool f64 = a.d.tune_upsert >= 3;
+    if (a.d.tune_upsert == 4 && !a.d.phased) {
+      k_upsert_p2md_rounds<true, 1, false, true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n,
+                                                                                a.uop >> 4, a.status,
+                                                                                a.conc_erase, a.gated);
+    } else if (a.d.phased) {
       if (f64) WS_UR(true, 1, true); else WS_UR(false, 1, true);
     } else {
       switch (a.d.tune_occ) {

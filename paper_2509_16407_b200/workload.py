@@ -85,16 +85,19 @@ def zipf_ranks(n: int, count: int, theta: float = 0.99, seed: int = 0) -> np.nda
 _BASE2 = np.array([0, 1, 2, 3], dtype=np.uint64)
 
 
-def kmer_keys(genome_len: int, k: int = 31, seed: int = 0) -> np.ndarray:
-    """Canonical k-mers of a seeded random genome, packed 2 bits/base, +1.
+def kmer_keys(genome_len: int, k: int = 31, seed: int = 0, repeats: int = 1) -> np.ndarray:
+    """Canonical k-mers of a seeded synthetic genome, packed 2 bits/base, +1.
 
+    The genome is `repeats` back-to-back copies of a random base sequence, so
+    every k-mer of the base occurs ~`repeats` times (known multiplicities).
     The +1 keeps every key clear of EMPTY_KEY (reference apps/tensor.py:119);
     k <= 31 keeps it below the RESERVED/TOMBSTONE sentinels.
     """
     if not 1 <= k <= 31:
         raise ValueError("k must be in [1, 31]")
     rng = np.random.default_rng(seed)
-    bases = rng.integers(0, 4, size=genome_len, dtype=np.uint64)
+    base = rng.integers(0, 4, size=max(k, genome_len // max(1, repeats)), dtype=np.uint64)
+    bases = np.tile(base, max(1, repeats))[:genome_len]
     n = genome_len - k + 1
     fwd = np.zeros(n, dtype=np.uint64)
     rev = np.zeros(n, dtype=np.uint64)

@@ -33,18 +33,21 @@ for design, cap in (("cuckoo", 1 << (22 if quick else 26)), ("chaining", 7 * (1 
     out[f"config4_sweep_{design}"] = r
     print("sweep", design, json.dumps(r)[:600], flush=True)
 
-r = runners.run_aging("iceberg_md", 1 << (22 if quick else 26), iterations=10 if quick else 40)
-rows += r.pop("rows")
-out["config3_aging_iceberg_md"] = r
-print("aging", json.dumps({k: v for k, v in r.items() if k != "iterations"}), flush=True)
+for comb in (True, False):
+    r = runners.run_aging("iceberg_md", 1 << (22 if quick else 26), iterations=10 if quick else 40, combine=comb)
+    rows += r.pop("rows")
+    out[f"config3_aging_iceberg_md_combine{int(comb)}"] = r
+    print("aging", json.dumps({k: v for k, v in r.items() if k != "iterations"}), flush=True)
 for d in ("iceberg_md", "iceberg", "unsafe_reference"):
     a = run_adversarial(d, buckets=100_000 if quick else 1_000_000, trials=3, seed=5, profile=DelayProfile.light())
     out[f"config3_adversarial_{d}"] = a
     print("adversarial", a, flush=True)
 
-r = runners.run_kmer(genome_len=1 << (22 if quick else 26), capacity=1 << (23 if quick else 27))
-out["config5_kmer_one_shard"] = r
-print("kmer", r, flush=True)
+for comb in (False, True):
+    r = runners.run_kmer(genome_len=1 << (22 if quick else 27), capacity=1 << (23 if quick else 26),
+                         repeats=4, combine=comb)
+    out[f"config5_kmer_one_shard_combine{int(comb)}"] = r
+    print("kmer", r, flush=True)
 out["seconds"] = time.time() - t0
 os.makedirs("profiles", exist_ok=True)
 tag = "quick" if quick else "r01"
