@@ -588,7 +588,7 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.wpn = 2 * c.bucket_size + 2;
   d.tune_qilp = 5;
   d.tune_l2pol = 2;
-  d.tune_upsert = 3;
+  d.tune_upsert = 4;
   d.tune_occ = 0;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };

@@ -49,8 +49,8 @@ for comb in (False, True):
     out[f"config5_kmer_one_shard_combine{int(comb)}"] = r
     print("kmer", r, flush=True)
 out["seconds"] = time.time() - t0
-os.makedirs("profiles", exist_ok=True)
+os.makedirs("gpurun_out", exist_ok=True)
 tag = "quick" if quick else "r01"
-json.dump(out, open(f"profiles/workloads_{tag}.json", "w"), indent=1, default=str)
-open(f"profiles/workloads_{tag}.csv", "w").write(render_csv(["one B200, paper_2509_16407_b200 runners"], rows))
+json.dump(out, open(f"gpurun_out/workloads_{tag}.json", "w"), indent=1, default=str)
+open(f"gpurun_out/workloads_{tag}.csv", "w").write(render_csv(["one B200, paper_2509_16407_b200 runners"], rows))
 print("done", out["seconds"])
