@@ -647,6 +647,10 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   }
   if (cudaEventCreateWithFlags(&t->ev_a, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
   if (cudaEventCreateWithFlags(&t->ev_b, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
+  t->L.preload(t->def_bs);
+  preload_fn(k_validate);
+  preload_fn(k_checksum);
+  cudaGetLastError();
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(WS_ERR_CUDA);
   *out = t;
   return WS_OK;

@@ -98,6 +98,14 @@ static void p2_md_query(const QueryArgs& a, bool def) {
 static void p2_md_locate(const LocateArgs& a, bool def) {
   if (def) launch_locate_t<D_P2_MD, 32>(a); else launch_locate_t<D_P2_MD, 0>(a);
 }
-Launchers launchers_p2_md() { return Launchers{p2_md_ops, p2_md_query, p2_md_locate}; }
+static void p2_md_preload(bool def) {
+  if (!def) { preload_t<D_P2_MD, 0>(); return; }
+  preload_t<D_P2_MD, 32>();
+  preload_fn(k_query_p2md_coop<false, true, 1>);
+  preload_fn(k_query_p2md_coop<true, true, 1>);
+  preload_fn(k_upsert_p2md_rounds<true, 1, false, true>);
+  preload_fn(k_upsert_p2md_rounds<true, 1, true>);
+}
+Launchers launchers_p2_md() { return Launchers{p2_md_ops, p2_md_query, p2_md_locate, p2_md_preload}; }
 
 }  // namespace ws

@@ -155,7 +155,23 @@ struct Launchers {
   void (*ops)(const OpsArgs&, bool default_bs);
   void (*query)(const QueryArgs&, bool default_bs);
   void (*locate)(const LocateArgs&, bool default_bs);
+  void (*preload)(bool default_bs);  // load every kernel now, not lazily inside a timed launch
 };
+
+template <class K>
+inline void preload_fn(K kernel) {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, kernel);
+}
+
+template <int DES, int BS>
+void preload_t() {
+  preload_fn(k_ops<DES, BS, false>);
+  preload_fn(k_ops<DES, BS, true>);
+  preload_fn(k_query<DES, BS, false>);
+  preload_fn(k_query<DES, BS, true>);
+  preload_fn(k_locate<DES, BS>);
+}
 
 #define WS_DEFINE_DESIGN(DES, NAME)                                                       \
   namespace ws {                                                                          \
@@ -168,7 +184,12 @@ struct Launchers {
   static void NAME##_locate(const LocateArgs& a, bool def) {                              \
     if (def) launch_locate_t<DES, default_bs(DES)>(a); else launch_locate_t<DES, 0>(a);   \
   }                                                                                       \
-  Launchers launchers_##NAME() { return Launchers{NAME##_ops, NAME##_query, NAME##_locate}; } \
+  static void NAME##_preload(bool def) {                                                   \
+    if (def) preload_t<DES, default_bs(DES)>(); else preload_t<DES, 0>();                 \
+  }                                                                                       \
+  Launchers launchers_##NAME() {                                                          \
+    return Launchers{NAME##_ops, NAME##_query, NAME##_locate, NAME##_preload};            \
+  }                                                                                       \
   }
 
 Launchers launchers_double();
