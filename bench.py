@@ -42,10 +42,12 @@ INSERT_TABLE_B = 64 + 64 * 0.232 + 32 + 32
 QUERY_TABLE_B = 116.0
 INSERT_IO_B = 17.0
 QUERY_IO_B = 17.0
-# L2-missing line requests per op (what the B200 random-access ceiling counts):
-# insert = primary tags 1 + alternate tags 0.232 + cell write 1; query =
-# 0.5 x (1 + 1 + 0.124) + 0.5 x 2 (positive / negative)
-INSERT_REQ = 2.232
+# Random DRAM line accesses per op, the unit of the B200 random-access ceiling
+# (scripts/gather_bench.cu: ~45 G/s; a dirtied line's write-back costs about
+# one more access, profiles/gather_sweep_r01.log):
+#   insert = primary tags 1 + alternate tags 0.232 + tag write-back 1 + cell
+#            write 1 = 3.232;  query = 0.5 x (1 + 1 + 0.124) + 0.5 x 2 = 2.062
+INSERT_REQ = 3.232
 QUERY_REQ = 2.062
 
 
@@ -364,7 +366,7 @@ def run_ours(args, rank, world):
                              "frac": round(qry_gbs / peak, 4),
                              "algorithmic_bytes_per_op": QUERY_TABLE_B + QUERY_IO_B},
             "random_access": {
-                "unit": "G L2-miss line requests/s",
+                "unit": "G random DRAM line accesses/s (reads + write-backs)",
                 "ceiling": ceiling,
                 "ceiling_source": "scripts/gather_bench.cu (profiles/ncu_traffic.json)",
                 "insert_requests_per_op": INSERT_REQ, "query_requests_per_op": QUERY_REQ,

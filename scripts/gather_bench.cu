@@ -57,6 +57,77 @@ __global__ void __launch_bounds__(256) gather(const char* buf, u64 nunits, u64 s
   if (acc == 0x123456789ull) out[0] = acc;
 }
 
+// random stores of W bytes (2, 16 or 32) at W-aligned positions
+template <int W, int R>
+__global__ void __launch_bounds__(256) scatter(char* buf, u64 nunits, u64 seed, int iters) {
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      const u64 idx = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) % nunits;
+      char* p = buf + idx * W;
+      if (W == 2) asm volatile("st.global.u16 [%0], %1;" :: "l"(p), "h"((unsigned short)tid) : "memory");
+      else if (W == 16) asm volatile("st.global.v2.u64 [%0], {%1, %2};" :: "l"(p), "l"(tid), "l"(idx) : "memory");
+      else asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" :: "l"(p), "l"(tid), "l"(idx), "l"(tid), "l"(idx) : "memory");
+    }
+  }
+}
+
+// random 64-byte read, then a write into the sector just read: MODE 0 none,
+// 1 a 2-byte store, 2 a full 32-byte sector store
+template <int MODE, int R>
+__global__ void __launch_bounds__(256) readwrite(char* buf, u64 nunits, u64 seed, int iters, u64* out) {
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  u64 acc = 0;
+  for (int it = 0; it < iters; it++) {
+    u64 a[R][4];
+    char* p[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      p[r] = buf + (mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) % nunits) * 64;
+      asm volatile("ld.relaxed.gpu.global.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
+                   : "=l"(a[r][0]), "=l"(a[r][1]), "=l"(a[r][2]), "=l"(a[r][3]) : "l"(p[r]) : "memory");
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      acc ^= a[r][0];
+      if (MODE == 1) asm volatile("st.global.u16 [%0], %1;" :: "l"(p[r] + 6), "h"((unsigned short)a[r][1]) : "memory");
+      if (MODE == 2) asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" :: "l"(p[r]), "l"(a[r][0] + 1), "l"(a[r][1]), "l"(a[r][2]), "l"(a[r][3]) : "memory");
+    }
+  }
+  if (acc == 7) out[0] = acc;
+}
+
+template <int MODE, int R>
+void run_rw(char* buf, u64 bytes, u64* out, int blocks, int iters, const char* name) {
+  const u64 nunits = bytes / 64;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  readwrite<MODE, R><<<blocks, 256>>>(buf, nunits, 1, 1, out);
+  cudaEventRecord(a);
+  readwrite<MODE, R><<<blocks, 256>>>(buf, nunits, 7, iters, out);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double acc = (double)blocks * 256 * R * iters;
+  printf("%-36s R=%d  %8.2f G ops/s\n", name, R, acc / ms / 1e6);
+}
+
+template <int W, int R>
+void run_st(char* buf, u64 bytes, int blocks, int iters, const char* name) {
+  const u64 nunits = bytes / W;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  scatter<W, R><<<blocks, 256>>>(buf, nunits, 1, 1);
+  cudaEventRecord(a);
+  scatter<W, R><<<blocks, 256>>>(buf, nunits, 7, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double acc = (double)blocks * 256 * R * iters;
+  printf("%-28s W=%4d R=%d  %8.2f G st/s  %8.1f GB/s useful\n", name, W, R, acc / ms / 1e6, acc * W / ms / 1e6);
+}
+
 template <int W, int FL, int R>
 void run(const char* buf, u64 bytes, u64* out, int blocks, int iters, const char* name) {
   const u64 nunits = bytes / W;
@@ -80,6 +151,20 @@ int main(int argc, char** argv) {
   cudaMalloc(&buf, bytes); cudaMalloc(&out, 64);
   cudaMemset(buf, 1, bytes);
   const int blocks = 148 * 8, iters = 16;
+  if (argc > 2 && argv[2][0] == 'r') {  // read-then-write-same-sector
+    run_rw<0, 4>(buf, bytes, out, blocks, iters, "read 32B only");
+    run_rw<1, 4>(buf, bytes, out, blocks, iters, "read 32B + 2B store same sector");
+    run_rw<2, 4>(buf, bytes, out, blocks, iters, "read 32B + 32B store same sector");
+    cudaDeviceSynchronize();
+    return 0;
+  }
+  if (argc > 2 && argv[2][0] == 'w') {  // random-store ceilings
+    run_st<2, 8>(buf, bytes, blocks, iters, "store 2B");
+    run_st<16, 8>(buf, bytes, blocks, iters, "store 16B");
+    run_st<32, 8>(buf, bytes, blocks, iters, "store 32B (full sector)");
+    cudaDeviceSynchronize();
+    return 0;
+  }
   if (argc > 2) {  // short sweep
     run<32, 1, 8>(buf, bytes, out, blocks, iters, "nc 32B");
     run<32, 3, 8>(buf, bytes, out, blocks, iters, "nc L2::64B 32B");
