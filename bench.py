@@ -199,8 +199,14 @@ def run_ours(args, rank, world):
     from paper_2509_16407_b200 import TableConfig, make_table
     from paper_2509_16407_b200.workload import derive_seed, gen_uniform_keys
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
     torch.cuda.set_device(dev)
+    host_coll = dist.is_initialized() and dist.get_backend() == "gloo"
+
+    def max_over_ranks(x):
+        t_ = torch.tensor([x], dtype=torch.float64, device="cpu" if host_coll else dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        return float(t_.item())
     slots = 1 << args.log2_slots
     if world > 1:
         # weak scaling: 2^log2_slots per GPU, one logical table hash-sharded over
@@ -270,9 +276,7 @@ def run_ours(args, rank, world):
     ms_ins = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     ms_qry = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
     if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = max_over_ranks(ms)
     ops_per_step = 2 * n * world
     value = ops_per_step * args.steps / (ms / 1000) / 1e6
 
@@ -305,9 +309,7 @@ def run_ours(args, rank, world):
     assert int((st_h == 1).sum()) == 0 and int((st_h == 2).sum()) <= 3
     e2e_s = statistics.median(e2e_times)
     if world > 1:
-        tt = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+        e2e_s = max_over_ranks(e2e_s)
     e2e_val = ops_per_step / e2e_s / 1e6
 
     if rank != 0:
@@ -391,8 +393,10 @@ def main():
     if world > 1 and args.impl == "ours":
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        # WS_DIST_BACKEND=gloo lets several ranks share one GPU (exchange staged
+        # through host memory) to exercise the sharded path without N GPUs
+        dist.init_process_group(os.environ.get("WS_DIST_BACKEND", "nccl"))
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

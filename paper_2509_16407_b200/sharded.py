@@ -91,20 +91,29 @@ class ShardedTable:
         self.router = router if router is not None else DeviceRouter(self.seed0, self.log2)
 
     # --------------------------------------------------------------- exchange
+    def _host_staged(self):
+        # gloo (CPU tests, or several ranks sharing one GPU) exchanges host tensors
+        import torch.distributed as dist
+        return dist.get_backend(self.group) == "gloo"
+
     def _counts(self, send_counts):
         import torch
         import torch.distributed as dist
-        recv = torch.empty_like(send_counts)
-        dist.all_to_all_single(recv, send_counts, group=self.group)
-        return recv
+        src = send_counts.cpu() if self._host_staged() else send_counts
+        recv = torch.empty_like(src)
+        dist.all_to_all_single(recv, src, group=self.group)
+        return recv.to(send_counts.device)
 
     def _a2a(self, t, recv_splits, send_splits):
         import torch
         import torch.distributed as dist
         view = t.view(torch.int64) if t.dtype == torch.uint64 else t
-        out = torch.empty(sum(recv_splits), dtype=view.dtype, device=t.device)
+        dev = view.device
+        if self._host_staged():
+            view = view.cpu()
+        out = torch.empty(sum(recv_splits), dtype=view.dtype, device=view.device)
         dist.all_to_all_single(out, view, recv_splits, send_splits, group=self.group)
-        return out.view(t.dtype)
+        return out.to(dev).view(t.dtype)
 
     def _route(self, keys, vals=None, ops=None):
         pk, pv, po, perm, counts = self.router.partition(keys, vals, ops)
@@ -162,7 +171,8 @@ class ShardedTable:
         import torch.distributed as dist
         if self.world == 1:
             return [list(vals)]
-        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(self.group) == "nccl" \
+            else "cpu"
         t = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v for v in vals], dtype=torch.int64,
                          device=dev)
         outs = [torch.empty_like(t) for _ in range(self.world)]
