@@ -176,6 +176,21 @@ WS_API int ws_partition(const uint64_t *keys, const uint64_t *vals, const uint8_
 WS_API int ws_unpermute(const void *in, const uint32_t *perm, uint64_t n, int elem_bytes, void *out,
                         void *stream);
 
+/* fused routing over NVLink peer memory (CUDA IPC): the routing kernel stores
+ * each op straight into its owner's inbox, owners apply it with the table
+ * kernels and store results straight back into the source's reply buffer.
+ * Collective: every rank calls ws_xchg_run with the same `rounds`
+ * (= ceil(max batch over ranks / chunk_ops)).  Device pointers only. */
+typedef struct ws_xchg ws_xchg;
+WS_API int ws_xchg_create(int world, int rank, uint64_t chunk_ops, int device, ws_xchg **out);
+WS_API int ws_xchg_handle(ws_xchg *x, void *handle_out /* 64 bytes */);
+WS_API int ws_xchg_open(ws_xchg *x, const void *handles /* world x 64 bytes, rank order */);
+WS_API int ws_xchg_run(ws_xchg *x, ws_table *local, const uint8_t *ops, uint8_t uop,
+                       const uint64_t *keys, const uint64_t *vals, uint64_t n, uint64_t rounds,
+                       uint64_t seed0, uint8_t *status, uint64_t *vals_out, void *stream,
+                       uint32_t flags);
+WS_API int ws_xchg_destroy(ws_xchg *x);
+
 WS_API const char *ws_strerror(int code);
 
 #ifdef __cplusplus

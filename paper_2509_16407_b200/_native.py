@@ -30,7 +30,8 @@ WS_F_COMBINE = 8
 EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_erase", "ws_mixed",
            "ws_locate", "ws_probe_counts", "ws_occupied", "ws_export_items",
            "ws_duplicate_scan", "ws_checksum", "ws_export_raw", "ws_info", "ws_tune",
-           "ws_partition", "ws_unpermute", "ws_strerror")
+           "ws_partition", "ws_unpermute", "ws_xchg_create", "ws_xchg_handle", "ws_xchg_open",
+           "ws_xchg_run", "ws_xchg_destroy", "ws_strerror")
 WS_TUNE_QUERY_ILP = 1
 WS_TUNE_L2_POLICY = 2
 WS_TUNE_UPSERT = 3
@@ -96,6 +97,11 @@ def load():
         lib.ws_tune.argtypes = [vp, i32, i32]
         lib.ws_partition.argtypes = [vp, vp, vp, u64, u64, i32, vp, vp, vp, vp, vp, vp]
         lib.ws_unpermute.argtypes = [vp, vp, u64, i32, vp, vp]
+        lib.ws_xchg_create.argtypes = [i32, i32, u64, i32, C.POINTER(vp)]
+        lib.ws_xchg_handle.argtypes = [vp, vp]
+        lib.ws_xchg_open.argtypes = [vp, vp]
+        lib.ws_xchg_run.argtypes = [vp, vp, vp, C.c_uint8, vp, vp, u64, u64, u64, vp, vp, vp, u32]
+        lib.ws_xchg_destroy.argtypes = [vp]
         lib.ws_strerror.argtypes = [i32]
         lib.ws_strerror.restype = C.c_char_p
         for name in EXPORTS:

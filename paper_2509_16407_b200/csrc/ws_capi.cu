@@ -528,6 +528,14 @@ int compact_items(ws_table* t, cudaStream_t s, ulonglong2** out, u64* count) {
 
 }  // namespace
 
+// internal (not exported): device-pointer batch execution for ws_shard.cu
+int ws_internal_run(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
+                    u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, bool query_only) {
+  if (cudaSetDevice(t->device) != cudaSuccess) return WS_ERR_CUDA;
+  return run_device(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only);
+}
+int ws_internal_device(ws_table* t) { return t->device; }
+
 // ===================================================================== C ABI
 
 extern "C" {

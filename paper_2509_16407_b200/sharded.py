@@ -7,9 +7,15 @@ local table indexes bucket bits 16..16+log2(nb), so owner and bucket are
 independent (SURVEY 8e).  The reference has no multi-GPU layer (SPEC.md:567);
 every batch op here is:
 
-    partition by owner (ws_partition)  ->  all_to_all_single of the keys
-    (+ values / op bytes)  ->  local batch op  ->  reverse all_to_all_single
-    of the results  ->  scatter back to the caller's order (ws_unpermute)
+    exchange="nccl": partition by owner (ws_partition) -> all_to_all_single
+    of the keys (+ values / op bytes) -> local batch op -> reverse
+    all_to_all_single of the results -> scatter back (ws_unpermute)
+
+    exchange="p2p": one routing kernel stores every op straight into its
+    owner's inbox over NVLink peer memory (CUDA IPC), owners apply their
+    inbox with the table kernels and store results straight back into the
+    source's reply buffer (ws_xchg_run) -- no partition buffer, no
+    collective call, no unpermute pass
 
 Each rank passes its own batch; results come back for that batch.  With one
 rank the exchange is skipped entirely.  The process group is the caller's
@@ -69,7 +75,8 @@ class DeviceRouter:
 class ShardedTable:
     """A table spread over all ranks of ``group``; batched ops only."""
 
-    def __init__(self, config: TableConfig, group=None, local_table=None, router=None, **table_kw):
+    def __init__(self, config: TableConfig, group=None, local_table=None, router=None,
+                 exchange: str = "nccl", chunk_ops: int = 1 << 24, **table_kw):
         import torch.distributed as dist
         cfg = validate_config(config)
         self.group = group
@@ -89,6 +96,60 @@ class ShardedTable:
         self.local = local_table
         self.seed0 = cfg.hash_family().seeds[0]
         self.router = router if router is not None else DeviceRouter(self.seed0, self.log2)
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' (all_to_all) or 'p2p' (fused NVLink stores)")
+        self.exchange = exchange
+        self._xchg = None
+        if exchange == "p2p" and self.world > 1:
+            self._open_p2p(chunk_ops)
+
+    # ------------------------------------------------- fused NVLink exchange
+    def _open_p2p(self, chunk_ops):
+        import torch
+        import torch.distributed as dist
+        from . import _native
+        lib = _native.load()
+        h = C.c_void_p()
+        dev = self.local.device.index
+        rc = lib.ws_xchg_create(self.world, self.rank, chunk_ops, dev, C.byref(h))
+        if rc:
+            raise RuntimeError(f"ws_xchg_create failed: {_native.strerror(rc)}")
+        self._xlib, self._xchg, self._chunk = lib, h, chunk_ops
+        mine = (C.c_char * 64)()
+        if lib.ws_xchg_handle(h, mine):
+            raise RuntimeError("ws_xchg_handle failed")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(mine), group=self.group)
+        blob = b"".join(handles)
+        if lib.ws_xchg_open(h, blob):
+            raise RuntimeError("ws_xchg_open failed (CUDA IPC / peer access)")
+        import weakref
+        self._xfin = weakref.finalize(self, lib.ws_xchg_destroy, h)
+        del torch
+
+    def _rounds(self, n):
+        import torch
+        import torch.distributed as dist
+        dev = "cpu" if self._host_staged() else self.local.device
+        t = torch.tensor([n], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return -(-int(t.item()) // self._chunk)
+
+    def _p2p(self, keys, vals, ops, uop, want_vals, check, merge_flags=0):
+        import torch
+        from . import _native
+        n = keys.numel()
+        dev = keys.device
+        status = torch.empty(n, dtype=torch.uint8, device=dev)
+        vout = torch.empty(n, dtype=torch.uint64, device=dev) if want_vals else None
+        fl = (_native.WS_F_SYNC_CHECK if check else _native.WS_F_NO_CHECK) | merge_flags
+        rc = self._xlib.ws_xchg_run(self._xchg, self.local._h, ops.data_ptr() if ops is not None else None,
+                                    uop, keys.data_ptr(), vals.data_ptr() if vals is not None else None, n,
+                                    self._rounds(n), self.seed0, status.data_ptr(),
+                                    vout.data_ptr() if vout is not None else None,
+                                    torch.cuda.current_stream(dev).cuda_stream, fl)
+        self.local._check(rc)
+        return status, vout
 
     # --------------------------------------------------------------- exchange
     def _host_staged(self):
@@ -133,6 +194,9 @@ class ShardedTable:
     def upsert_batch(self, keys, values, merge=None, check=True):
         if self.world == 1:
             return self.local.upsert_batch(keys, values, merge=merge, check=check)
+        if self._xchg is not None:
+            from .tables import OP_UPSERT, merge_id
+            return self._p2p(keys, values, None, OP_UPSERT | (merge_id(merge) << 4), False, check)[0]
         rk, rv, _ro, perm, send, recv = self._route(keys, values)
         st = self.local.upsert_batch(rk, rv, merge=merge, check=check)
         return self._back(st, perm, send, recv)
@@ -140,6 +204,10 @@ class ShardedTable:
     def query_batch(self, keys, check=True):
         if self.world == 1:
             return self.local.query_batch(keys, check=check)
+        if self._xchg is not None:
+            from .tables import OP_QUERY
+            st, vo = self._p2p(keys, None, None, OP_QUERY, True, check)
+            return st.bool(), vo
         rk, _rv, _ro, perm, send, recv = self._route(keys)
         found, vals = self.local.query_batch(rk, check=check)
         import torch
@@ -150,6 +218,9 @@ class ShardedTable:
     def erase_batch(self, keys, check=True):
         if self.world == 1:
             return self.local.erase_batch(keys, check=check)
+        if self._xchg is not None:
+            from .tables import OP_ERASE
+            return self._p2p(keys, None, None, OP_ERASE, False, check)[0].bool()
         rk, _rv, _ro, perm, send, recv = self._route(keys)
         import torch
         found = self.local.erase_batch(rk, check=check)
@@ -161,6 +232,8 @@ class ShardedTable:
             values = torch.zeros(keys.numel(), dtype=keys.dtype, device=keys.device)
         if self.world == 1:
             return self.local.mixed_batch(ops, keys, values, check=check)
+        if self._xchg is not None:
+            return self._p2p(keys, values, ops, 0, True, check)
         rk, rv, ro, perm, send, recv = self._route(keys, values, ops)
         st, vo = self.local.mixed_batch(ro, rk, rv, check=check)
         return self._back(st, perm, send, recv), self._back(vo, perm, send, recv)

@@ -36,7 +36,7 @@ def _np(t):
     return t.view(torch.int64).numpy().view(U64) if t.dtype == torch.uint64 else t.numpy()
 
 
-def _worker(rank, world, port, outq):
+def _worker(rank, world, port, outq, exchange="nccl"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         torch.cuda.set_device(0)
@@ -44,7 +44,8 @@ def _worker(rank, world, port, outq):
         from paper_2509_16407_b200 import TableConfig
         from paper_2509_16407_b200.sharded import ShardedTable
         from paper_2509_16407_b200.workload import gen_uniform_keys, mix64_np, zipf_ranks
-        st = ShardedTable(TableConfig(design="p2_md", capacity_slots=1 << 20, seed=42))
+        st = ShardedTable(TableConfig(design="p2_md", capacity_slots=1 << 20, seed=42), exchange=exchange,
+                          chunk_ops=1 << 16)
         n = 200_000
         mine = gen_uniform_keys(100 + rank, n)
         s = _np(st.upsert_batch(_cu(mine), _cu(mine & U64(0xFFFF))))
@@ -88,11 +89,16 @@ def _worker(rank, world, port, outq):
         raise
 
 
-def test_sharded_two_ranks_one_gpu_gloo():
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_sharded_two_ranks_one_gpu(exchange):
+    """exchange="nccl" runs the all-to-all path (gloo-staged here); "p2p"
+    runs the fused routing kernels over CUDA-IPC peer memory (two processes
+    on one device share it just like NVLink peers), with 2^16-op rounds so
+    the 200K-op batches take several rounds."""
     ctx = mp.get_context("spawn")
     outq = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, outq)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, outq, exchange)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(outq.get(timeout=600) for _ in procs)
