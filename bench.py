@@ -212,7 +212,9 @@ def run_ours(args, rank, world):
         # weak scaling: 2^log2_slots per GPU, one logical table hash-sharded over
         # all ranks; every batch is routed by owner with NCCL all-to-all
         from paper_2509_16407_b200.sharded import ShardedTable
-        table = ShardedTable(TableConfig(design=args.design, capacity_slots=slots * world, seed=42))
+        exchange = os.environ.get("WS_EXCHANGE", "p2p")
+        table = ShardedTable(TableConfig(design=args.design, capacity_slots=slots * world, seed=42),
+                             exchange=exchange)
     else:
         table = make_table(TableConfig(design=args.design, capacity_slots=slots, seed=42))
     n = int(slots * args.load)
@@ -352,7 +354,10 @@ def run_ours(args, rank, world):
                         f"{args.load} load, then {n} 50/50 hit/miss lock-free queries/GPU",
             "design": args.design, "log2_slots_per_gpu": args.log2_slots, "load": args.load,
             "ops_per_step": ops_per_step,
-            "parallelism": (f"hash-sharded x{world}: owner partition + NCCL all_to_all per batch"
+            "parallelism": ((f"hash-sharded x{world}: fused routing kernel stores ops into owners' "
+                             "inboxes over NVLink peer memory, results stored back directly"
+                             if table.exchange == "p2p" else
+                             f"hash-sharded x{world}: owner partition + all_to_all per batch")
                             if world > 1 else "1gpu"),
             "l2": "table 4.5 GiB and key batches 1.9 GiB exceed the 126 MB L2; no flush",
             "insert_ms": round(ms_ins, 3), "query_ms": round(ms_qry, 3),
@@ -380,7 +385,8 @@ def run_ours(args, rank, world):
         "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(n * 10),
                 "path": "ws_upsert/ws_query C ABI with pinned host buffers"},
-        "gpu_launches": (2 if world == 1 else 11) * args.steps,
+        "gpu_launches": (2 if world == 1 else (2 * (2 + 2 * world + 3)
+                                                 if table.exchange == "p2p" else 11)) * args.steps,
         "clocks": clk.report(),
     }
     print(json.dumps(out), flush=True)
