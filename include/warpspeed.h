@@ -60,6 +60,7 @@ extern "C" {
 #define WS_ERR_ALLOC (-4)
 #define WS_ERR_ARG (-5)
 #define WS_ERR_INVALID_OP (-6)
+#define WS_ERR_TIMEOUT (-7)     /* a peer rank never arrived at a device barrier */
 
 /* designs (same order as reference core.py:40-50 DESIGNS) */
 enum {

@@ -549,6 +549,7 @@ const char* ws_strerror(int code) {
     case WS_ERR_ALLOC: return "device allocation failed";
     case WS_ERR_ARG: return "invalid argument";
     case WS_ERR_INVALID_OP: return "invalid op byte (kind > 2 or merge > 4)";
+    case WS_ERR_TIMEOUT: return "a peer rank never reached the exchange barrier (60 s)";
     default: return "unknown error";
   }
 }

@@ -162,6 +162,7 @@ int ws_internal_run(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u
 namespace {
 
 constexpr int kMaxWorld = 8;
+constexpr u64 kWaitLimitNs = 60ull * 1000 * 1000 * 1000;  // a peer silent for 60 s is gone
 
 struct XRegion {  // byte offsets inside a rank's region
   u64 keys, vals, src, ops, incoming, res_st, res_vo, rep_st, rep_vo, bar, total;
@@ -250,11 +251,23 @@ __global__ void k_xs_send(XPeers peers, XRegion L, int world, int rank, int shif
   }
 }
 
-__global__ void k_xs_wait(u64* bar, u64 target) {
+// Bounded device-side wait: a rank that never arrives (crashed peer) must not
+// hang the GPU; after `limit_ns` the kernel records a timeout and returns.
+__device__ __forceinline__ u64 globaltimer_ns() {
+  u64 t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__global__ void k_xs_wait(u64* bar, u64 target, u64 limit_ns, u32* timed_out) {
   unsigned ns = 32;
+  const u64 t0 = globaltimer_ns();
   while (ld_acquire_sys(bar) < target) {
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
+    if (globaltimer_ns() - t0 > limit_ns) {
+      atomicExch(timed_out, 1u);
+      return;
+    }
   }
 }
 
@@ -314,7 +327,7 @@ WS_API int ws_xchg_create(int world, int rank, uint64_t chunk_ops, int device, w
   if (cudaMalloc((void**)&x->region, x->L.total) != cudaSuccess) { delete x; return WS_ERR_ALLOC; }
   cudaMemset(x->region, 0, x->L.total);
   if (cudaMalloc((void**)&x->scratch, 64 * 4) != cudaSuccess) { cudaFree(x->region); delete x; return WS_ERR_ALLOC; }
-  cudaMallocHost((void**)&x->h_counts, 8 * kMaxWorld);
+  cudaMallocHost((void**)&x->h_counts, 8 * (kMaxWorld + 1));
   for (int i = 0; i < kMaxWorld; i++) x->peers.base[i] = nullptr;
   x->peers.base[rank] = x->region;
   *out = x;
@@ -387,11 +400,14 @@ WS_API int ws_xchg_run(ws_xchg* x, ws_table* local, const uint8_t* ops, uint8_t 
     k_xs_send<<<(unsigned)g, 256, 0, s>>>(x->peers, L, W, x->rank, shift, x->C, seed0, (const u64*)keys,
                                           (const u64*)vals, ops, uop, lo, m, x->scratch, x->scratch + 8);
     x->epoch += W;
-    k_xs_wait<<<1, 1, 0, s>>>((u64*)(x->region + L.bar), x->epoch);
+    k_xs_wait<<<1, 1, 0, s>>>((u64*)(x->region + L.bar), x->epoch, kWaitLimitNs, x->scratch + 10);
     // 2. apply each source segment locally
     if (cudaMemcpyAsync(x->h_counts, x->region + L.incoming, 8 * W, cudaMemcpyDeviceToHost, s) != cudaSuccess)
       return WS_ERR_CUDA;
+    if (cudaMemcpyAsync(x->h_counts + kMaxWorld, x->scratch + 10, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return WS_ERR_CUDA;
     if (cudaStreamSynchronize(s) != cudaSuccess) return WS_ERR_CUDA;
+    if (*(const u32*)(x->h_counts + kMaxWorld)) return WS_ERR_TIMEOUT;
     for (int src = 0; src < W && rc == WS_OK; src++) {
       const u64 ns = x->h_counts[src];
       if (!ns) continue;
@@ -407,7 +423,7 @@ WS_API int ws_xchg_run(ws_xchg* x, ws_table* local, const uint8_t* ops, uint8_t 
     k_xs_reply<<<148 * 4, 256, 0, s>>>(x->peers, L, W, x->C, (const u64*)(x->region + L.incoming), x->region,
                                        x->scratch + 9, want_vals ? 1 : 0);
     x->epoch += W;
-    k_xs_wait<<<1, 1, 0, s>>>((u64*)(x->region + L.bar), x->epoch);
+    k_xs_wait<<<1, 1, 0, s>>>((u64*)(x->region + L.bar), x->epoch, kWaitLimitNs, x->scratch + 10);
     if (m) {
       if (status && cudaMemcpyAsync(status + lo, x->region + L.rep_st, m, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return WS_ERR_CUDA;
@@ -417,6 +433,12 @@ WS_API int ws_xchg_run(ws_xchg* x, ws_table* local, const uint8_t* ops, uint8_t 
     }
   }
   if (rc == WS_OK && cudaGetLastError() != cudaSuccess) rc = WS_ERR_CUDA;
+  if (rc == WS_OK) {
+    if (cudaMemcpyAsync(x->h_counts + kMaxWorld, x->scratch + 10, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return WS_ERR_CUDA;
+    if (*(const u32*)(x->h_counts + kMaxWorld)) rc = WS_ERR_TIMEOUT;
+  }
   return rc;
 }
 
