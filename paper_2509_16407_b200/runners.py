@@ -278,3 +278,53 @@ def run_kmer(genome_len: int = 1 << 24, k: int = 31, capacity: int = 1 << 25, de
     ok = bool(_np(found).all() and (_np(vals) == c.astype(U64)).all())
     return {"kmers": len(km), "distinct": len(u), "load": len(u) / t.capacity_slots, "ok": ok,
             "ms": ms, "mops": _mops(len(km), ms), "occupied": t.occupied_count()}
+
+
+YCSB_MIX = {"A": 0.50, "B": 0.05, "C": 0.0}  # update fraction (reference apps/ycsb.py:21)
+
+
+def run_ycsb(workload: str, universe: int = 1 << 24, ops: int = 1 << 26, capacity: int = 0,
+             design: str = "p2_md", theta: float = 0.99, seed: int = 42, batch: int = 1 << 24,
+             combine: bool = True) -> dict:
+    """YCSB A/B/C on the device table (reference apps/ycsb.py:37-93): the
+    universe is preloaded (values k & 0xFFFF), keys are Zipf(theta) ranks,
+    one update every 1/ratio ops (REPLACE with value i & 0xFFFFFFFF), the rest
+    queries.  Each chunk of `batch` ops is one mixed launch.  Every query must
+    hit; with combining (stable sort keeps index order) the final values are
+    exactly those of the reference's sequential run (last update wins)."""
+    from .tables import OP_QUERY, OP_UPSERT, make_table
+    frac = YCSB_MIX[workload]
+    cap = capacity or int(universe / 0.85) // 32 * 32
+    t = make_table(TableConfig(design=design, capacity_slots=cap, seed=seed))
+    dev = t.device
+    keys = gen_uniform_keys(seed, universe)
+    st = t.upsert_batch(_dev(keys, dev), _dev(keys & U64(0xFFFF), dev))
+    if int((_np(st) != 0).sum()):
+        raise RuntimeError("YCSB preload did not insert every key")
+    period = round(1 / frac) if frac else 0
+    ranks = zipf_ranks(universe, ops, theta, seed=derive_seed(seed, 1)) - 1
+    idx = np.arange(ops, dtype=np.int64)
+    is_up = (idx % period == 0) if period else np.zeros(ops, dtype=bool)
+    op_b = np.where(is_up, OP_UPSERT, OP_QUERY).astype(np.uint8)  # merge 0 = REPLACE
+    ks = keys[ranks]
+    vs = (idx.astype(np.uint64) & U64(0xFFFFFFFF))
+    ms, missing = 0.0, 0
+    t.mixed_batch(_dev(op_b[:4096], dev), _dev(ks[:4096], dev), _dev(vs[:4096], dev), combine=combine)  # warm
+    for lo in range(0, ops, batch):
+        hi = min(ops, lo + batch)
+        d_o, d_k, d_v = _dev(op_b[lo:hi], dev), _dev(ks[lo:hi], dev), _dev(vs[lo:hi], dev)
+        with _Timer() as tm:
+            s, _v = t.mixed_batch(d_o, d_k, d_v, check=False, combine=combine)
+        ms += tm.ms
+        s = _np(s)
+        missing += int((~is_up[lo:hi] & (s == 0)).sum())
+    # model of the final values: preload, then the last update of each key in index order
+    final = keys & U64(0xFFFF)
+    if period:
+        up_i = np.nonzero(is_up)[0]
+        final[ranks[up_i]] = vs[up_i]  # fancy assignment keeps the last write per index
+    found, vals = t.query_batch(_dev(keys, dev))
+    values_ok = bool(_np(found).all() and (_np(vals) == final).all()) if combine else bool(_np(found).all())
+    return {"workload": workload, "universe": universe, "ops": ops, "updates": int(is_up.sum()),
+            "ms": ms, "mops": _mops(ops, ms), "missing_queries": missing, "final_values_exact": values_ok,
+            "combine": combine}

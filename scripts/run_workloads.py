@@ -48,6 +48,10 @@ for comb in (False, True):
                          repeats=4, combine=comb)
     out[f"config5_kmer_one_shard_combine{int(comb)}"] = r
     print("kmer", r, flush=True)
+for wl in ("A", "B", "C"):
+    r = runners.run_ycsb(wl, universe=1 << (20 if quick else 24), ops=1 << (22 if quick else 26))
+    out[f"ycsb_{wl}"] = r
+    print("ycsb", r, flush=True)
 out["seconds"] = time.time() - t0
 os.makedirs("gpurun_out", exist_ok=True)
 tag = "quick" if quick else "r01"

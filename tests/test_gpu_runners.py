@@ -34,3 +34,10 @@ def test_kmer_counts():
     from paper_2509_16407_b200 import runners
     r = runners.run_kmer(genome_len=1 << 18, capacity=1 << 19)
     assert r["ok"], r
+
+
+@pytest.mark.parametrize("wl", ["A", "B", "C"])
+def test_ycsb_final_values_exact(wl):
+    from paper_2509_16407_b200 import runners
+    r = runners.run_ycsb(wl, universe=1 << 16, ops=1 << 18, batch=1 << 16)
+    assert r["missing_queries"] == 0 and r["final_values_exact"], r
