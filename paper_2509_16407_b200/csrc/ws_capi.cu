@@ -281,6 +281,11 @@ __global__ void k_comb_iota(u64 n, u32* idx) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) idx[i] = (u32)i;
 }
 
+__global__ void k_comb_gather(const u64* keys, const u32* order, u64 n, u64* out) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x)
+    out[j] = keys[order[j]];
+}
+
 __global__ void k_comb_heads(const u64* sk, const u32* si, const u8* ops, u8 uop, const u64* vals, u64 n,
                              u32* head, OpVal* ov) {
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
@@ -343,14 +348,32 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   WS_CK(cudaMallocAsync((void**)&agg, sizeof(OpVal) * n, s));
   WS_CK(cudaMallocAsync((void**)&nruns, 8, s));
   k_comb_iota<<<grid_for(n), kThreads, 0, s>>>(n, idx);
-  size_t tb = 0, tb2 = 0, tb3 = 0;
+  // runs must be contiguous per (key, op byte) even when a key's upserts are
+  // interleaved with other ops: for mixed batches a stable pre-sort by op
+  // byte, then a stable sort by key (LSD order) -> (key, op, index) order
+  u8 *op_sorted = nullptr;
+  u64* keys_by_op = nullptr;
+  const u64* sort_keys = keys;
+  size_t tb0 = 0, tb = 0, tb2 = 0, tb3 = 0;
+  if (ops) {
+    WS_CK(cudaMallocAsync((void**)&op_sorted, n, s));
+    WS_CK(cudaMallocAsync((void**)&keys_by_op, 8 * n, s));
+    cub::DeviceRadixSort::SortPairs(nullptr, tb0, ops, op_sorted, idx, si, (int64_t)n, 0, 8, s);
+  }
   cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
   cub::DeviceScan::InclusiveSum(nullptr, tb2, head, seg, (int64_t)n, s);
   cub::DeviceReduce::ReduceByKey(nullptr, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
   void* tmp = nullptr;
-  const size_t tmax = std::max(tb, std::max(tb2, tb3)) + 16;
+  const size_t tmax = std::max(std::max(tb0, tb), std::max(tb2, tb3)) + 16;
   WS_CK(cudaMallocAsync(&tmp, tmax, s));
-  cub::DeviceRadixSort::SortPairs(tmp, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
+  if (ops) {
+    // idx -> si ordered by op (stable); gather keys in that order; si -> idx
+    cub::DeviceRadixSort::SortPairs(tmp, tb0, ops, op_sorted, idx, si, (int64_t)n, 0, 8, s);
+    k_comb_gather<<<grid_for(n), kThreads, 0, s>>>(keys, si, n, keys_by_op);
+    WS_CK(cudaMemcpyAsync(idx, si, 4 * n, cudaMemcpyDeviceToDevice, s));
+    sort_keys = keys_by_op;
+  }
+  cub::DeviceRadixSort::SortPairs(tmp, tb, sort_keys, sk, idx, si, (int64_t)n, 0, 64, s);
   k_comb_heads<<<grid_for(n), kThreads, 0, s>>>(sk, si, ops, uop, vals, n, head, ov);
   cub::DeviceScan::InclusiveSum(tmp, tb2, head, seg, (int64_t)n, s);
   cub::DeviceReduce::ReduceByKey(tmp, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
@@ -372,8 +395,9 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
     rc = cuda_err(cudaGetLastError());
   }
   for (void* p : {(void*)sk, (void*)idx, (void*)si, (void*)head, (void*)seg, (void*)uniq, (void*)ov, (void*)agg,
-                  (void*)nruns, tmp, (void*)gkey, (void*)gval, (void*)gvo, (void*)gop, (void*)gst})
-    cudaFreeAsync(p, s);
+                  (void*)nruns, tmp, (void*)gkey, (void*)gval, (void*)gvo, (void*)gop, (void*)gst,
+                  (void*)op_sorted, (void*)keys_by_op})
+    if (p) cudaFreeAsync(p, s);
   return rc;
 }
 
