@@ -39,6 +39,16 @@ Launchers launchers_for(int design) {
 
 // ------------------------------------------------------------------ kernels
 
+// mixed batches: count erase ops so the op kernel enables the concurrent-erase
+// (fenced tombstone-flag) path only when the batch really erases
+__global__ void k_count_erases(const u8* __restrict__ ops, u64 n, u32* state) {
+  u32 c = 0;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    c += (__ldg(ops + i) & 15) == OP_ERASE;
+  c = __reduce_add_sync(0xFFFFFFFFu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(state + 4, c);
+}
+
 __global__ void k_validate(const u64* __restrict__ keys, const u8* __restrict__ ops, u64 n, u32* state) {
   u32 bad_k = 0, bad_o = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
@@ -224,7 +234,13 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
   if (rc) return rc;
   if (!n) return WS_OK;
   const int gated = (flags & WS_F_NO_CHECK) ? 0 : 1;
-  const int conc = (has_erase || t->cfg.multi_stream) ? 1 : 0;
+  int conc = (has_erase || t->cfg.multi_stream) ? 1 : 0;
+  if (ops && !t->cfg.multi_stream && !(flags & WS_F_SERIAL)) {
+    // let the device decide: conc_erase = 2 reads the erase count at launch
+    WS_CK(cudaMemsetAsync(t->d.state + 4, 0, sizeof(u32), s));
+    k_count_erases<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(ops, n, t->d.state);
+    conc = 2;
+  }
   if (query_only && !(flags & WS_F_SERIAL)) {
     QueryArgs qa{t->d, keys, n, vout, status, conc, gated, t->cfg.phased ? 1 : 0, s};
     t->L.query(qa, t->def_bs);

@@ -49,7 +49,9 @@ __global__ void __launch_bounds__(kThreads) k_ops(Dev d, const u8* __restrict__ 
   Probe* pp = nullptr;
   Probe pr;
   if constexpr (INSTR) pp = &pr;
-  Ctx<DES, BS, false, INSTR> c{d, pp, conc_erase != 0, ld_u32_relaxed(d.state)};
+  // conc_erase 2: the launch's erase count (k_count_erases) decides
+  const bool conc = conc_erase == 2 ? ld_u32_relaxed(d.state + 4) != 0 : conc_erase != 0;
+  Ctx<DES, BS, false, INSTR> c{d, pp, conc, ld_u32_relaxed(d.state)};
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     if (redo && redo[i] != S_RETRY) continue;
     const u8 op = ops ? __ldg(ops + i) : uop;
