@@ -757,6 +757,43 @@ struct Ctx {
     return -1;
   }
 
+  // Depth-1 prefix of the reference BFS (cuckoo.py:107-156) without a
+  // workspace: start buckets in order, their resident slots in order, seeds
+  // in order, skipping alternates already seen; the first alternate with a
+  // free slot is exactly the path the full BFS returns when one of length 1
+  // exists.  1: found (move in mv[0..3]), 0: no length-1 path (run the full
+  // BFS), -1: seen set overflowed the local budget (run the full BFS).
+  __device__ int ck_find_path1(const u64* uq, int nu, u64* mv) {
+    constexpr int kSeen = 96;
+    u64 seen[kSeen];
+    int ns = 0;
+    for (int i = 0; i < nu; i++) seen[ns++] = uq[i];
+    const int n = B();
+    for (int i = 0; i < nu; i++) {
+      const u64 bucket = uq[i];
+      for (int j = 0; j < n; j++) {
+        const u64 slot = bucket * (u64)n + j;
+        u64 k, v;
+        ldc(slot, k, v);
+        if (k == EMPTY || k >= RESV) continue;
+        for (int sd = 0; sd < d.ways; sd++) {
+          const u64 alt = hb(sd, k, d.nbm);
+          if (alt == bucket) continue;
+          bool dup = false;
+          for (int q = 0; q < ns && !dup; q++) dup = seen[q] == alt;
+          if (dup) continue;
+          if (find_free(alt * (u64)n, n) >= 0) {
+            mv[0] = bucket; mv[1] = slot; mv[2] = k; mv[3] = alt;
+            return 1;
+          }
+          if (ns == kSeen) return -1;
+          seen[ns++] = alt;
+        }
+      }
+    }
+    return 0;
+  }
+
   // reference cuckoo.py:158-183, deepest move first, each under {src, dst}
   __device__ bool ck_execute(const u64* mv, int len) {
     const int n = B();
@@ -806,6 +843,14 @@ struct Ctx {
       ck_unlock_all(uq, nu);
       if (st != 0xFF) return st;
       if (free_at >= 0) continue;  // lost a race for the free cell: retry
+      if (d.depth >= 1) {
+        u64 mv1[4];
+        const int r1 = ck_find_path1(uq, nu, mv1);
+        if (r1 == 1) {
+          ck_execute(mv1, 1);  // a failed move means the world changed: retry
+          continue;
+        }
+      }
       u32 wid;
       u64* ws = ws_acquire(wid);
       const int len = ck_find_path(ws, uq, nu);

@@ -112,6 +112,7 @@ def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_
     neg = gen_uniform_keys(derive_seed(seed, 0xFEED), query_sample)
     rows, points, fulls = [], [], 0
     placed = 0
+    inserted_mask = np.ones(n_max, dtype=bool)
     t.query_batch(_dev(neg[:4096], dev), check=False)  # first-launch costs outside the timed region
     for point in load_points:
         target = int(cap * point)
@@ -122,16 +123,21 @@ def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_
         d_timed = _dev(timed, dev)  # H2D outside the timed region
         with _Timer() as ti:
             st = t.upsert_batch(d_timed, d_timed, check=False)
-        fulls += int((_np(st) == 2).sum())
+        st_np = _np(st)
+        fulls += int((st_np == 2).sum())
+        if (st_np == 2).any():  # FULLed keys are legitimately absent: keep them out of the hit set
+            inserted_mask[placed:placed + len(timed)] &= st_np != 2
         ins_probe = 0.0
         if np_ins:
             pst, _v, pr, _l = t.probe_batch(np.full(np_ins, OP_UPSERT, np.uint8), batch[-np_ins:],
                                             batch[-np_ins:], serial=False)
             fulls += int((pst == 2).sum())
+            inserted_mask[target - np_ins:target] &= pst != 2
             ins_probe = float(pr.mean())
         placed = target
         qn = min(query_sample, placed)
-        pos = keys[:placed][np.linspace(0, placed - 1, qn // 2).astype(np.int64)]
+        live_keys = keys[:placed][inserted_mask[:placed]]
+        pos = live_keys[np.linspace(0, len(live_keys) - 1, qn // 2).astype(np.int64)]
         q = np.concatenate([pos, neg[: qn - len(pos)]])
         d_q = _dev(q, dev)
         with _Timer() as tq:
@@ -153,7 +159,7 @@ def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_
                        "probes_insert": ins_probe, "probes_query_pos": float(prp.mean()),
                        "probes_query_neg": float(prn.mean()), "queries_ok": ok, "fulls_so_far": fulls})
     if drain:
-        live = keys[:placed]
+        live = keys[:placed][inserted_mask[:placed]]
         chunk = -(-len(live) // 18)
         for off in range(0, len(live), chunk):
             sl = live[off:off + chunk]
