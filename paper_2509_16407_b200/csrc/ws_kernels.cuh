@@ -163,7 +163,12 @@ struct Launchers {
 template <class K>
 inline void preload_fn(K kernel) {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, kernel);
+  if (cudaFuncGetAttributes(&a, kernel) != cudaSuccess) return;
+  // reserve the per-thread local memory now: growing the context's local
+  // pool later happens synchronously inside some unrelated timed launch
+  size_t cur = 0;
+  if (cudaDeviceGetLimit(&cur, cudaLimitStackSize) == cudaSuccess && cur < a.localSizeBytes)
+    cudaDeviceSetLimit(cudaLimitStackSize, a.localSizeBytes);
 }
 
 template <int DES, int BS>
