@@ -11,6 +11,8 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <thread>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -147,6 +149,7 @@ struct ws_table {
   u64* h_pin;  // pinned scratch (64 words)
   cudaStream_t s_aux, s_in;
   cudaEvent_t ev_a, ev_b, ev_in;
+  std::vector<cudaEvent_t> ev_chunk;  // per-chunk H2D completion (staged mutations)
 };
 
 namespace {
@@ -424,6 +427,43 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
 // reported after the fact.  Mutating batches must be validated in full before
 // the first mutation: all chunks are copied and validated (overlapped), one
 // sync reads the verdict, then compute and D2H overlap chunk by chunk.
+// Sentinel / op-byte scan of host-resident batch inputs on all host cores
+// (same rule as k_validate): WS_OK, WS_ERR_INVALID_KEY or WS_ERR_INVALID_OP.
+int host_validate(const u64* keys, const u8* ops, u64 n) {
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = std::max(1u, std::min(nt, 16u));
+  if (n < ((u64)1 << 20)) nt = 1;
+  std::vector<int> res(nt, WS_OK);
+  auto work = [&](unsigned w) {
+    const u64 lo = n * w / nt, hi = n * (w + 1) / nt;
+    for (u64 b = lo; b < hi; b += 4096) {
+      const u64 e = std::min(hi, b + 4096);
+      u64 bad = 0;
+      for (u64 i = b; i < e; i++) bad |= (u64)(keys[i] - 1 >= 0xFFFFFFFFFFFFFFFDull);  // 0, 2^64-2, 2^64-1
+      if (bad) { res[w] = WS_ERR_INVALID_KEY; return; }
+      if (ops) {
+        u32 bo = 0;
+        for (u64 i = b; i < e; i++) bo |= (u32)((ops[i] & 15) > OP_QUERY) | (u32)((ops[i] >> 4) > M_MIN);
+        if (bo) res[w] = WS_ERR_INVALID_OP;  // keep scanning: a bad key anywhere wins
+      }
+    }
+  };
+  if (nt == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (unsigned w = 1; w < nt; w++) th.emplace_back(work, w);
+    work(0);
+    for (auto& x : th) x.join();
+  }
+  int rc = WS_OK;
+  for (int r : res) {
+    if (r == WS_ERR_INVALID_KEY) return r;
+    if (r) rc = r;
+  }
+  return rc;
+}
+
 int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                bool query_only) {
@@ -482,16 +522,43 @@ int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
       if (!rc) rc = d2h(off, m);
     }
   } else {
-    for (u64 off = 0; off < n && rc == WS_OK; off += chunk) rc = h2d(off, std::min(chunk, n - off));
-    if (!rc && check) {
+    // A mutation may not start before the WHOLE batch is validated (the
+    // reference rejects a batch with a sentinel key before any op runs).
+    // Host-resident inputs are validated on the host, by all cores, WHILE
+    // the copy engine streams them in; each chunk's compute then starts as
+    // soon as its own copy lands, so the kernels hide under the H2D stream.
+    const u64 nch = (n + chunk - 1) / chunk;
+    while (t->ev_chunk.size() < nch) {
+      cudaEvent_t e;
+      WS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      t->ev_chunk.push_back(e);
+    }
+    for (u64 c = 0; c < nch; c++) {
+      const u64 off = c * chunk, m = std::min(chunk, n - off);
+      if (hk) WS_CK(cudaMemcpyAsync((void*)(dk + off), keys + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
+      if (hv) WS_CK(cudaMemcpyAsync((void*)(dv + off), vals + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
+      if (ho) WS_CK(cudaMemcpyAsync((void*)(dops + off), ops + off, m, cudaMemcpyHostToDevice, t->s_in));
+      WS_CK(cudaEventRecord(t->ev_chunk[c], t->s_in));
+    }
+    if (check && hk && (!ops || ho)) {
+      rc = host_validate(keys, ho ? ops : nullptr, n);
+    } else if (check) {
+      for (u64 c = 0; c < nch; c++) {
+        const u64 off = c * chunk, m = std::min(chunk, n - off);
+        WS_CK(cudaStreamWaitEvent(s, t->ev_chunk[c], 0));
+        k_validate<<<grid_for(m, kThreads, 4), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
+                                                                 t->d.state);
+      }
+      WS_CK(cudaGetLastError());
       WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 2, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
       WS_CK(cudaStreamSynchronize(s));
       const u32* c = (const u32*)t->h_pin;
       if (c[0]) rc = WS_ERR_INVALID_KEY;
       else if (c[1]) rc = WS_ERR_INVALID_OP;
     }
-    for (u64 off = 0; off < n && rc == WS_OK; off += chunk) {
-      const u64 m = std::min(chunk, n - off);
+    for (u64 c = 0; c < nch && rc == WS_OK; c++) {
+      const u64 off = c * chunk, m = std::min(chunk, n - off);
+      WS_CK(cudaStreamWaitEvent(s, t->ev_chunk[c], 0));
       rc = compute(off, m);
       if (!rc) rc = d2h(off, m);
     }
@@ -721,6 +788,7 @@ int ws_destroy(ws_table* t) {
   if (t->s_aux) cudaStreamDestroy(t->s_aux);
   if (t->s_in) cudaStreamDestroy(t->s_in);
   if (t->ev_in) cudaEventDestroy(t->ev_in);
+  for (cudaEvent_t e : t->ev_chunk) cudaEventDestroy(e);
   if (t->ev_a) cudaEventDestroy(t->ev_a);
   if (t->ev_b) cudaEventDestroy(t->ev_b);
   delete t;

@@ -29,6 +29,7 @@ import ctypes as C
 import dataclasses
 
 from .core import ConfigError, TableConfig, validate_config
+from .tables import as_bool
 
 
 class DeviceRouter:
@@ -207,24 +208,24 @@ class ShardedTable:
         if self._xchg is not None:
             from .tables import OP_QUERY
             st, vo = self._p2p(keys, None, None, OP_QUERY, True, check)
-            return st.bool(), vo
+            return as_bool(st), vo
         rk, _rv, _ro, perm, send, recv = self._route(keys)
         found, vals = self.local.query_batch(rk, check=check)
         import torch
         found = self._back(found.to(torch.uint8), perm, send, recv)
         vals = self._back(vals, perm, send, recv)
-        return found.bool(), vals
+        return as_bool(found), vals
 
     def erase_batch(self, keys, check=True):
         if self.world == 1:
             return self.local.erase_batch(keys, check=check)
         if self._xchg is not None:
             from .tables import OP_ERASE
-            return self._p2p(keys, None, None, OP_ERASE, False, check)[0].bool()
+            return as_bool(self._p2p(keys, None, None, OP_ERASE, False, check)[0])
         rk, _rv, _ro, perm, send, recv = self._route(keys)
         import torch
         found = self.local.erase_batch(rk, check=check)
-        return self._back(found.to(torch.uint8), perm, send, recv).bool()
+        return as_bool(self._back(found.to(torch.uint8), perm, send, recv))
 
     def mixed_batch(self, ops, keys, values=None, check=True):
         import torch

@@ -134,6 +134,12 @@ def _as_u8(x, torch):
     return a, a.ctypes.data, False
 
 
+def as_bool(t):
+    """0/1 uint8 flags as a bool tensor without a conversion pass (zero-copy view)."""
+    import torch
+    return t.view(torch.bool) if t.dtype == torch.uint8 else t.bool()
+
+
 def _checked_out(t, n, dtype):
     if t.numel() != n or not t.is_contiguous() or t.element_size() != dtype.itemsize:
         raise ValueError(f"out tensor must be contiguous with {n} elements of {dtype}")
@@ -432,7 +438,7 @@ class HashTable:
         fl = _native.WS_F_SYNC_CHECK if check else _native.WS_F_NO_CHECK
         self._check(self._lib.ws_query(self._h, kp, len(k), vals.data_ptr(), found.data_ptr(),
                                        self._stream(), fl))
-        return found.bool(), vals
+        return as_bool(found), vals
 
     def erase_batch(self, keys, check=True):
         torch = _torch()
@@ -441,7 +447,7 @@ class HashTable:
         self._dirty()
         fl = _native.WS_F_SYNC_CHECK if check else _native.WS_F_NO_CHECK
         self._check(self._lib.ws_erase(self._h, kp, len(k), found.data_ptr(), self._stream(), fl))
-        return found.bool()
+        return as_bool(found)
 
     def mixed_batch(self, ops, keys, values=None, check=True, serial=False, combine=False):
         """One launch of mixed ops (byte = kind | merge << 4, kind 0 upsert /

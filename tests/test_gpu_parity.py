@@ -245,6 +245,43 @@ def test_host_buffers_roundtrip_through_cabi():
     np.testing.assert_array_equal(_np(vals)[:50_000], keys ^ np.uint64(77))
 
 
+def test_host_staged_multichunk_pipeline_and_validation():
+    """Host batches larger than one staging chunk (4M ops): the mutation
+    compute pipelines behind the H2D copies after a host-side (threaded)
+    validation; a sentinel key or bad op byte anywhere rejects the whole
+    batch before any op runs."""
+    from paper_2509_16407_b200 import InvalidKeyError
+    cfg = cfg_for("p2_md", 1 << 24, seed=3)
+    t = _table(cfg)
+    n = 9_000_000
+    keys = _keys(11, n)
+    vals = keys ^ np.uint64(5)
+    st = t.upsert_batch(keys, vals)
+    assert not st.is_cuda and (st.numpy() == 0).all()
+    before = t.checksum()
+    assert before[0] == n
+    for pos in (0, 4_194_303, 4_194_304, n - 1):
+        for bad in (0, U64, U64 - 1):
+            k2 = _keys(12, n)
+            k2[pos] = bad
+            with pytest.raises(InvalidKeyError):
+                t.upsert_batch(k2, k2)
+    assert t.checksum() == before
+    ops = np.zeros(n, dtype=np.uint8)
+    ops[n - 3] = 0x03  # kind 3 does not exist
+    with pytest.raises(Exception):
+        t.mixed_batch(ops, _keys(13, n), _keys(13, n))
+    assert t.checksum() == before
+    found, got = t.query_batch(keys)
+    assert found.numpy().all()
+    np.testing.assert_array_equal(_np(got), vals)
+    # the same host batch twice: every op is now an update
+    st = t.upsert_batch(keys, vals, merge="add")
+    assert (st.numpy() == 1).all()
+    found, got = t.query_batch(keys[:1000])
+    np.testing.assert_array_equal(_np(got), vals[:1000] * np.uint64(2))
+
+
 def test_chaining_grows_past_nominal_capacity():
     cfg = cfg_for("chaining", 7 * 64, seed=1)
     t = _table(cfg)
