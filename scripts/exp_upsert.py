@@ -29,4 +29,7 @@ for up, occ in variants:
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ins = int((st == 0).sum())
-    print(f"upsert={up} occ={occ}: ms={min(ts[1:]):.2f} {['%.2f' % x for x in ts]} inserted={ins}/{n}", flush=True)
+    f, got = t.query_batch(keys, check=False)
+    ok = bool(f.all()) and bool((got == vals).all())
+    print(f"upsert={up} occ={occ}: ms={min(ts[1:]):.2f} {['%.2f' % x for x in ts]} inserted={ins}/{n} "
+          f"query_ok={ok} checksum={t.checksum()} dups={t.duplicate_count()}", flush=True)
