@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include "warpspeed.h"
+#include "ws_bulk.cuh"
 #include "ws_kernels.cuh"
 
 using namespace ws;
@@ -150,6 +151,9 @@ struct ws_table {
   cudaStream_t s_aux, s_in;
   cudaEvent_t ev_a, ev_b, ev_in;
   std::vector<cudaEvent_t> ev_chunk;  // per-chunk H2D completion (staged mutations)
+  bool maybe_tomb;  // an erase may have run since creation / clear (host hint for the bulk path)
+  int tune_bulk;    // WS_TUNE_BULK: 0 off, 1 auto, 2 always when eligible
+  int tune_bulk_gb; // WS_TUNE_BULK_GROUP: buckets per group log2 (-1 = from the batch density)
 };
 
 namespace {
@@ -229,6 +233,25 @@ int chain_grow(ws_table* t, cudaStream_t s) {
 }
 
 // Run one batch whose buffers are all device-resident.
+// Bucket-partitioned bulk upsert (ws_bulk.cu): P2-MD with default buckets,
+// uniform upsert batches much larger than the bucket count, tables whose
+// launches are not concurrent across streams (phase A relies on ownership, not
+// locks) and that never tombstoned (phase A is the shortcut regime).
+bool bulk_eligible(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u32 flags, cudaStream_t s) {
+  if (t->cfg.design != D_P2_MD || !t->def_bs || (uop & 15) != OP_UPSERT || t->tune_bulk == 0) return false;
+  if ((flags & WS_F_SERIAL) || t->cfg.multi_stream || t->cfg.phased || t->d.lock_elided) return false;
+  if (n >= (1ull << 32) || !bulk_aligned(keys, vals)) return false;
+  if (t->tune_bulk == 1 && (n < (1ull << 20) || n < 4 * t->d.nb)) return false;
+  if (t->maybe_tomb) {  // an erase ran: ask the device whether it ever tombstoned
+    if (cudaMemcpyAsync(t->h_pin, t->d.state, sizeof(u32), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return false;
+    if (*(const u32*)t->h_pin) return false;
+    t->maybe_tomb = false;
+  }
+  return true;
+}
+
 int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                      bool query_only) {
@@ -237,6 +260,13 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
   if (rc) return rc;
   if (!n) return WS_OK;
   const int gated = (flags & WS_F_NO_CHECK) ? 0 : 1;
+  if (has_erase) t->maybe_tomb = true;
+  if (!query_only && !ops && bulk_eligible(t, uop, keys, vals, n, flags, s)) {
+    BulkPlan plan = bulk_plan(n, t->d.nb, t->tune_bulk_gb);
+    plan.skip_b = t->tune_bulk == 3;
+    plan.cap = std::max(0, t->d.shortcut - 4);
+    return cuda_err(bulk_upsert_p2md(t->d, keys, vals, n, uop >> 4, status, gated, s, plan));
+  }
   int conc = (has_erase || t->cfg.multi_stream) ? 1 : 0;
   if (ops && !t->cfg.multi_stream && !(flags & WS_F_SERIAL)) {
     // let the device decide: conc_erase = 2 reads the erase count at launch
@@ -706,6 +736,9 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.tune_l2pol = 2;
   d.tune_upsert = 4;
   d.tune_occ = 0;
+  t->tune_bulk = 0;  // measured slower than the per-op kernel at 2^28
+  t->tune_bulk_gb = -1;
+  t->maybe_tomb = false;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };
   if (c.design == D_CHAINING) {
@@ -804,6 +837,7 @@ int ws_clear(ws_table* t, void* stream) {
   if (d.tags) WS_CK(cudaMemsetAsync(d.tags, 0, d.cap * 2, s));
   WS_CK(cudaMemsetAsync(d.locks, 0, t->lock_words * 4, s));
   WS_CK(cudaMemsetAsync(d.state, 0, N_STATE * 4, s));
+  t->maybe_tomb = false;
   if (t->cfg.design == D_CHAINING) {
     t->h_pin[0] = d.nb + 1;
     WS_CK(cudaMemcpyAsync(d.chain_next, t->h_pin, 8, cudaMemcpyHostToDevice, s));
@@ -1033,6 +1067,14 @@ int ws_tune(ws_table* t, int knob, int value) {
       return WS_OK;
     case WS_TUNE_DELAY_SEED:
       t->d.delay_seed = mix64((u64)(unsigned)value);
+      return WS_OK;
+    case WS_TUNE_BULK:
+      if (value < 0 || value > 3) return WS_ERR_ARG;
+      t->tune_bulk = value;
+      return WS_OK;
+    case WS_TUNE_BULK_GROUP:
+      if (value < -1 || value > 8) return WS_ERR_ARG;
+      t->tune_bulk_gb = value;
       return WS_OK;
     case WS_TUNE_UPSERT:
       if (value < 0 || value > 4) return WS_ERR_ARG;

@@ -1,5 +1,6 @@
 // Kernel instantiations for the p2_md design (the headline path): the generic
 // kernels of ws_kernels.cuh plus the tuned multi-lookup query of ws_fast.cuh.
+#include "ws_bulk.cuh"
 #include "ws_fast.cuh"
 #include "ws_kernels.cuh"
 
@@ -105,7 +106,14 @@ static void p2_md_preload(bool def) {
   preload_fn(k_query_p2md_coop<true, true, 1>);
   preload_fn(k_upsert_p2md_rounds<true, 1, false, true>);
   preload_fn(k_upsert_p2md_rounds<true, 1, true>);
+  bulk_preload();
 }
+void bulk_phase_b(const Dev& d, const BulkRec* recs, u64 n_max, int merge, u8* status, int gated,
+                  const u64* n_dev, unsigned grid, cudaStream_t s) {
+  k_upsert_p2md_rounds<true, 1, false, true, true><<<grid, 256, 0, s>>>(
+      d, nullptr, nullptr, n_max, merge, status, 0, gated, reinterpret_cast<const u64*>(recs), n_dev);
+}
+
 Launchers launchers_p2_md() { return Launchers{p2_md_ops, p2_md_query, p2_md_locate, p2_md_preload}; }
 
 }  // namespace ws

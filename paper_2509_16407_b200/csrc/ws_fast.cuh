@@ -372,6 +372,30 @@ __global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __re
   }
 }
 
+// Pseudo-random bijection of [0, n): a 4-round balanced Feistel network on
+// `bits` (even, 2^bits >= n) bits keyed by `key`, cycle-walked back into
+// range (expected < 4 steps).  Bulk phase B visits its deferred records in
+// this order: the records are bucket-sorted, and any structured visiting
+// order (bucket order, group order, even a golden-ratio Weyl stride once
+// ~10^5 ops run concurrently) leaves measurable FULLs in a 0.9 fill that a
+// random order does not.
+__device__ __forceinline__ u64 feistel_perm(u64 x, u64 n, int bits, u64 key) {
+  const int h = bits >> 1;
+  const u64 m = (1ull << h) - 1;
+  do {
+    u64 l = x >> h, r = x & m;
+#pragma unroll
+    for (int rd = 0; rd < 4; rd++) {
+      const u64 f = mix64(r ^ (key + (u64)rd * 0x9E3779B97F4A7C15ull)) & m;
+      const u64 t = l ^ f;
+      l = r;
+      r = t;
+    }
+    x = (l << h) | r;
+  } while (x >= n);
+  return x;
+}
+
 // =============================================== warp-synchronous rounds
 //
 // P2-MD upsert, one thread per op, in warp-synchronous lock rounds.  A
@@ -505,22 +529,43 @@ __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64*
 // under the bucket lock; storing (0,0) there too makes the 32-byte sector
 // fully valid in L2, so its eviction needs no ECC read-modify-write of the
 // untouched half (measured ~1 DRAM sector per insert without it).
-template <bool F64, int MINB, bool PHASED, bool FILL = false>
+template <bool F64, int MINB, bool PHASED, bool FILL = false, bool REC = false>
 __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, int merge,
-                                                            u8* status, int conc_erase, int gated) {
+                                                            u8* status, int conc_erase, int gated,
+                                                            const u64* __restrict__ recs = nullptr,
+                                                            const u64* n_dev = nullptr) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  // bulk phase B (ws_bulk.cu): ops are 32-byte records (key, value, batch
+  // index, pad) counted on the device (n_dev[0]) and visited in a
+  // pseudo-random order (feistel_perm), statuses other than INSERTED
+  // (pre-filled) scattered to the batch index
+  if constexpr (REC) n = *n_dev;
   const u32 te0 = ld_u32_relaxed(d.state);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
-  for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c * 32 < n; c += nwarps) {
+  const u64 c0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  int pbits = 0;
+  if constexpr (REC) {
+    while ((1ull << pbits) < n) pbits++;
+    pbits += pbits & 1;
+  }
+  for (u64 c = c0; c * 32 < n; c += nwarps) {
     const u64 i = c * 32 + lane;
     bool pending = i < n;
-    u64 key = 0, val = 0, b0 = 0, b1 = 0;
+    u64 key = 0, val = 0, b0 = 0, b1 = 0, sidx = 0;
     u16 tag = 1;
     if (pending) {
-      key = __ldg(keys + i);
-      val = __ldg(vals + i);
+      if constexpr (REC) {
+        const u64 pj = feistel_perm(i, n, pbits, d.seeds[2]);
+        const ulonglong2 r0 = __ldg(reinterpret_cast<const ulonglong2*>(recs + 4 * pj));
+        key = r0.x;
+        val = r0.y;
+        sidx = __ldg(recs + 4 * pj + 2);
+      } else {
+        key = __ldg(keys + i);
+        val = __ldg(vals + i);
+      }
       const u64 h0 = mix64(key ^ d.seeds[0]);
       b0 = d.nbm(h0 >> 16);
       const u16 t = (u16)(h0 & 0xFFFF);
@@ -613,7 +658,10 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
         if (backoff < 4096) backoff <<= 1;
       }
     }
-    if (i < n && status) status[i] = st;
+    if (i < n && status) {
+      if constexpr (!REC) status[i] = st;
+      else if (st != S_INSERTED) status[sidx] = st;
+    }
   }
 }
 

@@ -1,0 +1,185 @@
+"""GPU parity of the bucket-partitioned bulk upsert (csrc/ws_bulk.cu).
+
+The bulk path executes a batch as "phase A (shortcut inserts and b0 hits,
+bucket by bucket in batch order), then phase B (the locked per-op kernel over
+the deferred ops)" -- one valid serial order of the batch (reference
+tables/openaddr.py:370-418).  Checked against the oracle on identical inputs:
+per-op statuses where the batch order cannot matter, the final key->value
+map, query hit/miss sets and values, zero duplicates.  `tune(bulk=2)` forces
+the path at test sizes; `bulk_group` forces group shapes that need one, two
+or three partition passes.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import cfg_for
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _keys(seed, n):
+    from paper_2509_16407_b200.workload import gen_uniform_keys
+    return gen_uniform_keys(seed, n)
+
+
+def _cuda(a):
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint8:
+        return torch.from_numpy(a).cuda()
+    return torch.from_numpy(a.astype(np.uint64, copy=False).view(np.int64)).cuda().view(torch.uint64)
+
+
+def _np(t):
+    return t.cpu().view(torch.int64).numpy().view(np.uint64) if t.dtype == torch.uint64 else t.cpu().numpy()
+
+
+def _pair(cap, seed=42, bulk=2, group=None):
+    from oracle import OracleTable
+    from paper_2509_16407_b200 import make_table
+    cfg = cfg_for("p2_md", cap, seed=seed)
+    t = make_table(cfg)
+    t.tune(bulk=bulk, bulk_group=group)
+    return t, OracleTable(cfg), cfg
+
+
+def _check_queries(t, o, keys, miss):
+    q = np.concatenate([keys, miss])
+    found, got = t.query_batch(_cuda(q))
+    ofound, oval = o.query_batch(q)
+    np.testing.assert_array_equal(_np(found).astype(bool), ofound)
+    np.testing.assert_array_equal(_np(got), oval)
+
+
+@pytest.mark.parametrize("cap,group", [(1 << 16, None), (1 << 16, 0), (1 << 18, None), (32 * 3001, None),
+                                       (1 << 22, None), (1 << 20, 8)])
+def test_bulk_fill_matches_oracle(cap, group):
+    """One batch from empty to 0.9 load: every status INSERTED, same map as
+    the sequential oracle, every key found, no absent key found."""
+    t, o, cfg = _pair(cap, group=group)
+    n = int(cfg.capacity_slots * 0.9)
+    keys = _keys(42, n)
+    vals = keys & np.uint64(0xFFFF)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals)))
+    ost = o.upsert_batch(keys, vals)
+    assert not (ost != 0).any(), "ill-posed: oracle hit FULL"
+    np.testing.assert_array_equal(st, ost)
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_count() == 0
+    _check_queries(t, o, keys[::3], _keys(7, 20_000))
+
+
+def test_bulk_three_partition_passes():
+    """2^21 single-bucket groups need 21 group bits -> three LSD passes."""
+    t, o, cfg = _pair(1 << 26, group=0)
+    n = int(cfg.capacity_slots * 0.5)
+    keys = _keys(5, n)
+    vals = keys * np.uint64(3)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals)))
+    assert (st == 0).all()
+    with np.errstate(over="ignore"):
+        assert t.checksum()[:3] == (n, int(keys.sum(dtype=np.uint64)), int(vals.sum(dtype=np.uint64)))
+    found, got = t.query_batch(_cuda(keys[::97]))
+    assert bool(found.all())
+    np.testing.assert_array_equal(_np(got), vals[::97])
+    assert t.duplicate_count() == 0
+
+
+@pytest.mark.parametrize("merge", [None, "add", "max", "min", "keep"])
+def test_bulk_incremental_batches_statuses_exact(merge):
+    """Four batches of distinct keys mixing re-upserts of present keys with
+    fresh ones: per-op statuses (UPDATED vs INSERTED) and the merged values
+    equal the oracle's -- exercises the pre-existing-cell confirm path."""
+    t, o, cfg = _pair(1 << 18)
+    cap = cfg.capacity_slots
+    fresh = _keys(11, int(cap * 0.9))
+    rng = np.random.default_rng(1)
+    done = 0
+    for i, frac in enumerate((0.3, 0.25, 0.2, 0.15)):
+        m = int(cap * frac)
+        new = fresh[done:done + m]
+        old = fresh[:done][rng.random(done) < 0.4] if done else fresh[:0]
+        keys = np.concatenate([new, old])
+        keys = keys[rng.permutation(len(keys))]
+        vals = (keys * np.uint64(0x9E3779B97F4A7C15) + np.uint64(i)) >> np.uint64(8)
+        st = _np(t.upsert_batch(_cuda(keys), _cuda(vals), merge=merge))
+        ost = o.upsert_batch(keys, vals, merge)
+        np.testing.assert_array_equal(st, ost)
+        done += m
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_count() == 0
+    _check_queries(t, o, fresh[: done : 5], _keys(8, 10_000))
+
+
+@pytest.mark.parametrize("merge", ["add", "max", "min"])
+def test_bulk_zipf_duplicates_commutative(merge):
+    """Zipf(0.99) hot keys, many same-key ops per bucket in one batch: the
+    same-key folding of phase A and the deferred duplicates of phase B give
+    the oracle's map and exactly one INSERTED per distinct key."""
+    from paper_2509_16407_b200.workload import zipf_ranks
+    t, o, cfg = _pair(1 << 16, seed=5)
+    uni = _keys(12, int(cfg.capacity_slots * 0.85))
+    keys = uni[zipf_ranks(len(uni), 400_000, 0.99, seed=4) - 1]
+    vals = (np.arange(len(keys), dtype=np.uint64) * np.uint64(2654435761)) & np.uint64(0xFFFFFF)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals), merge=merge))
+    o.upsert_batch(keys, vals, merge)
+    assert not (st == 2).any()
+    assert dict(t.items()) == o.as_dict()
+    assert int((st == 0).sum()) == len(np.unique(keys))
+    assert t.duplicate_count() == 0
+
+
+@pytest.mark.parametrize("merge", [None, "keep"])
+def test_bulk_duplicates_order_dependent_merges(merge):
+    """REPLACE / KEEP with duplicate keys in one batch: every key holds one
+    of its batch values (the serial order of phase B is unspecified), one
+    INSERTED per distinct key, no FULL, no duplicates."""
+    t, _o, cfg = _pair(1 << 16, seed=6)
+    uni = _keys(13, 40_000)
+    keys = uni[np.random.default_rng(2).integers(0, len(uni), 120_000)]
+    vals = np.arange(len(keys), dtype=np.uint64) + np.uint64(1)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals), merge=merge))
+    assert int((st == 0).sum()) == len(np.unique(keys)) and not (st == 2).any()
+    per = {}
+    for k, v in zip(keys.tolist(), vals.tolist()):
+        per.setdefault(k, set()).add(v)
+    got = dict(t.items())
+    assert set(got) == set(per) and all(got[k] in per[k] for k in got)
+    assert t.duplicate_count() == 0
+
+
+def test_bulk_off_after_erase_still_exact():
+    """After an erase the table has tombstoned: the bulk path must step aside
+    (shortcut regime gone) and results stay exact."""
+    t, o, cfg = _pair(1 << 16, seed=8)
+    keys = _keys(3, int(cfg.capacity_slots * 0.6))
+    t.upsert_batch(_cuda(keys), _cuda(keys))
+    o.upsert_batch(keys, keys)
+    gone = t.erase_batch(_cuda(keys[:5000]))
+    o.erase_batch(keys[:5000])
+    assert bool(gone.all())
+    more = _keys(4, int(cfg.capacity_slots * 0.3))
+    st = _np(t.upsert_batch(_cuda(more), _cuda(more)))
+    ost = o.upsert_batch(more, more)
+    np.testing.assert_array_equal(st, ost)
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_count() == 0
+
+
+def test_bulk_and_per_op_paths_agree():
+    """Same inputs through the bulk path and the per-op kernel: same map."""
+    from paper_2509_16407_b200 import make_table
+    cfg = cfg_for("p2_md", 1 << 20, seed=77)
+    keys = _keys(21, int(cfg.capacity_slots * 0.9))
+    vals = keys >> np.uint64(3)
+    maps, checks = [], []
+    for bulk in (0, 2):
+        t = make_table(cfg)
+        t.tune(bulk=bulk)
+        st = _np(t.upsert_batch(_cuda(keys), _cuda(vals), merge="add"))
+        assert (st == 0).all()
+        checks.append(t.checksum())
+        maps.append(dict(t.items()))
+    assert checks[0] == checks[1] and maps[0] == maps[1]
