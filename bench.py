@@ -359,7 +359,8 @@ def run_ours(args, rank, world):
                              if table.exchange == "p2p" else
                              f"hash-sharded x{world}: owner partition + all_to_all per batch")
                             if world > 1 else "1gpu"),
-            "l2": "table 4.5 GiB and key batches 1.9 GiB exceed the 126 MB L2; no flush",
+            "l2": (f"table {18 * slots / 2**30:.1f} GiB and key batches {8 * n / 2**30:.1f} GiB exceed "
+                   "the 126 MB L2; no flush"),
             "insert_ms": round(ms_ins, 3), "query_ms": round(ms_qry, 3),
             "full_statuses_first_step": fulls,
             "insert_mops": round(n / ms_ins / 1e3, 1), "query_mops": round(n / ms_qry / 1e3, 1),
