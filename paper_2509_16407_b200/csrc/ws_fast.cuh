@@ -574,9 +574,28 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
     }
     u8 st = 0;
     unsigned backoff = 64;
+    // Locks a lane holds across rounds.  Retries must not be symmetric: two
+    // lanes of one warp that each hold their primary and want the other's
+    // (b1(A) = b0(B), b1(B) = b0(A)) would fail, release and collide again in
+    // every lockstep round -- a livelock, hit in tombstoned small tables where
+    // every insert needs its alternate.  The first attempt try-locks b1 in any
+    // order (non-blocking, so no deadlock); after a failure a lane only ever
+    // waits for a HIGHER bucket while holding a lower one: holding b0 it
+    // retries b1 > b0 next round without releasing b0; needing b1 < b0 it
+    // releases b0 and next round takes b1 first, then b0 (`lofirst`).
+    bool held0 = false, held1 = false, lofirst = false;
     while (__any_sync(0xFFFFFFFFu, pending)) {
-      // phase 1: try-lock the primary (never blocks)
-      const bool hold0 = pending && (PHASED || try_lock_bucket(d.locks, b0));
+      // phase 1: try-locks in ascending order (never block)
+      if (!PHASED && pending) {
+        if (lofirst) {
+          if (!held1) held1 = try_lock_bucket(d.locks, b1);
+          if (held1 && !held0) held0 = try_lock_bucket(d.locks, b0);
+        } else if (!held0) {
+          held0 = try_lock_bucket(d.locks, b0);
+        }
+      }
+      const bool hold0 = pending && (PHASED || held0);
+      bool drop0 = false;
       // phase 2: primary tag blocks, one request per op
       u32 M0, Z0;
       coop_masks<false, F64>(d, hold0, b0, tag, M0, Z0);
@@ -596,8 +615,19 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
           const int zc0 = __popc(Z0);
           used0 = 32 - (zc0 < d.zcc ? zc0 : d.zcc);
           if ((te || used0 >= d.shortcut) && b1 != b0) {
-            hold1 = PHASED || try_lock_bucket(d.locks, b1);
-            need1 = hold1;  // a failed try-lock retries the whole op next round
+            if (PHASED || held1) {
+              hold1 = true;
+            } else {
+              held1 = try_lock_bucket(d.locks, b1);
+              hold1 = held1;
+              // on failure: b1 above b0 -> keep b0 and retry b1 next round;
+              // b1 below b0 -> release b0, next round take b1 first, then b0
+              if (!held1 && b1 < b0) {
+                lofirst = true;
+                drop0 = true;
+              }
+            }
+            need1 = hold1;
           } else {
             decided = true;  // shortcut (or b1 == b0): the primary it is
           }
@@ -646,12 +676,19 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
           }
         }
       }
-      // phase 4: one MEMBAR for the warp, then relaxed releases
+      // phase 4: one MEMBAR for the warp, then relaxed releases of the
+      // finished lanes' locks (pending lanes keep what they hold, see above)
       if (!PHASED) {
         __syncwarp();
         fence_acq_rel();
-        if (hold1) red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
-        if (hold0) red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+        if (held1 && !pending) {
+          red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
+          held1 = false;
+        }
+        if (held0 && (!pending || drop0)) {
+          red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+          held0 = false;
+        }
       }
       if (pending) {
         __nanosleep(backoff + 8 * (threadIdx.x & 31));

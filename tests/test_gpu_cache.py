@@ -1,0 +1,63 @@
+"""Batched device cache simulator (paper_2509_16407_b200/cache.py) against
+the reference CacheSim's contract (apps/cache.py): every get returns the
+dataset value, the table mirrors the FIFO ring, nothing is lost, the load
+stays <= 0.85, and under uniform access the hit rate tracks the
+cache-to-data ratio (cache.py:100-107)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "double"])
+def test_cache_values_conservation_and_hit_rate(design):
+    from paper_2509_16407_b200.cache import DeviceCacheSim
+    from paper_2509_16407_b200.core import TableConfig
+    from paper_2509_16407_b200.tables import make_table
+    from paper_2509_16407_b200.workload import gen_uniform_keys
+    n = 1 << 14
+    keys = gen_uniform_keys(3, n)
+    vals = keys ^ np.uint64(0x5555)
+
+    def d(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda().view(torch.uint64)
+
+    backing = make_table(TableConfig(design="p2_md", capacity_slots=1 << 15, seed=9))
+    assert int((backing.upsert_batch(d(keys), d(vals)) != 0).sum()) == 0
+    ratio = 0.25
+    slots = (int(n * ratio / 0.85) + 2 + 31) // 32 * 32
+    table = make_table(TableConfig(design=design, capacity_slots=slots, seed=4))
+    sim = DeviceCacheSim(table, backing, capacity=int(n * ratio))
+    for lo in range(0, sim.capacity, 512):
+        sim.get_batch(d(keys[lo:min(lo + 512, sim.capacity)]))
+    sim.hits = sim.misses = 0
+    idx = np.random.default_rng(1).integers(0, n, size=4 * n)
+    for lo in range(0, len(idx), 512):
+        got = sim.get_batch(d(keys[idx[lo:lo + 512]]))
+        np.testing.assert_array_equal(got.cpu().view(torch.int64).numpy().view(np.uint64), vals[idx[lo:lo + 512]])
+    hit = sim.hits / (sim.hits + sim.misses)
+    assert abs(hit - ratio) < 0.05, hit
+    assert sim.evictions > 0
+    sim.check_conservation(keys)
+    assert len(sim.resident_keys()) == sim.capacity
+
+
+def test_cache_rejects_unstable_design():
+    from paper_2509_16407_b200.cache import CacheError, DeviceCacheSim
+    from paper_2509_16407_b200.core import TableConfig
+    from paper_2509_16407_b200.tables import make_table
+    t = make_table(TableConfig(design="cuckoo", capacity_slots=1 << 12, seed=1))
+    b = make_table(TableConfig(design="p2_md", capacity_slots=1 << 12, seed=1))
+    with pytest.raises(CacheError):
+        DeviceCacheSim(t, b)
+
+
+def test_cache_sweep_runner():
+    from paper_2509_16407_b200.cache import run_cache_sweep
+    res = run_cache_sweep(universe=1 << 15, ratios=(0.1, 0.5), queries_per_key=2.0, batch=1 << 12)
+    for r in res:
+        assert r["values_exact"]
+        assert abs(r["hit_rate"] - r["ratio"]) < 0.05, r

@@ -407,3 +407,28 @@ def test_combined_hot_key_batch_matches_oracle(design, merge):
             per.setdefault(k, set()).add(v)
         assert set(got) == set(per) and all(got[k] in per[k] for k in got)
     assert t.duplicate_scan() == {}
+
+
+def test_tombstoned_small_table_upserts_make_progress():
+    """After erases the shortcut is off, so every P2-MD insert locks its
+    alternate bucket too; in a small table lanes of one warp cross-lock each
+    other's buckets (b1(A) = b0(B), b1(B) = b0(A)).  The lock-round upsert
+    kernel must make progress (regression: symmetric try-lock retries
+    livelocked in lockstep) and stay exact against the oracle."""
+    cfg = cfg_for("p2_md", 1 << 12, seed=3)
+    t = _table(cfg)
+    o = _oracle(cfg)
+    keys = _keys(5, 2900)
+    t.upsert_batch(_cuda(keys), _cuda(keys))
+    o.upsert_batch(keys, keys)
+    gone = t.erase_batch(_cuda(keys[:1450]))
+    o.erase_batch(keys[:1450])
+    assert bool(gone.all())
+    for r in range(8):
+        new = _keys(100 + r, 180)
+        st = _np(t.upsert_batch(_cuda(new), _cuda(new), merge="keep"))
+        ost = o.upsert_batch(new, new, "keep")
+        assert not (ost == 2).any(), "ill-posed: oracle hit FULL"
+        np.testing.assert_array_equal(st, ost)
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
