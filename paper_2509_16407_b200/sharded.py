@@ -102,7 +102,25 @@ class ShardedTable:
         self.exchange = exchange
         self._xchg = None
         if exchange == "p2p" and self.world > 1:
-            self._open_p2p(chunk_ops)
+            # collective decision: every rank must use the same exchange, so a
+            # rank that cannot map its peers (no CUDA IPC / peer access) moves
+            # the whole group to the NCCL all-to-all path
+            err = None
+            try:
+                self._open_p2p(chunk_ops)
+            except RuntimeError as e:  # noqa: PERF203
+                err = e
+            import torch
+            flag = torch.tensor([0 if err is None else 1], dtype=torch.int64,
+                                device="cpu" if self._host_staged() else self.local.device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+            if int(flag.item()):
+                if self._xchg is not None:
+                    self._xfin()
+                    self._xchg = None
+                self.exchange = "nccl"
+                import warnings
+                warnings.warn(f"p2p exchange unavailable on some rank ({err or 'peer failure'}); using nccl")
 
     # ------------------------------------------------- fused NVLink exchange
     def _open_p2p(self, chunk_ops):
@@ -116,6 +134,8 @@ class ShardedTable:
         if rc:
             raise RuntimeError(f"ws_xchg_create failed: {_native.strerror(rc)}")
         self._xlib, self._xchg, self._chunk = lib, h, chunk_ops
+        import weakref
+        self._xfin = weakref.finalize(self, lib.ws_xchg_destroy, h)
         mine = (C.c_char * 64)()
         if lib.ws_xchg_handle(h, mine):
             raise RuntimeError("ws_xchg_handle failed")
@@ -124,8 +144,6 @@ class ShardedTable:
         blob = b"".join(handles)
         if lib.ws_xchg_open(h, blob):
             raise RuntimeError("ws_xchg_open failed (CUDA IPC / peer access)")
-        import weakref
-        self._xfin = weakref.finalize(self, lib.ws_xchg_destroy, h)
         del torch
 
     def _rounds(self, n):
