@@ -432,3 +432,50 @@ def test_tombstoned_small_table_upserts_make_progress():
         np.testing.assert_array_equal(st, ost)
     assert dict(t.items()) == o.as_dict()
     assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("design,log2", [("p2_md", 16), ("p2_md", 22), ("iceberg_md", 16), ("double", 16),
+                                         ("cuckoo", 16), ("chaining", 12)])
+def test_multi_stream_concurrent_launches(design, log2):
+    """multi_stream tables: upsert-ADD (two streams, overlapping keys), erase
+    and query launches run concurrently on four CUDA streams.  Roles are
+    key-disjoint between erase / query / upsert and ADD is commutative, so the
+    outcome is order-independent: every query hits with its value, every
+    erase succeeds, the final map equals the oracle's, no duplicates."""
+    cfg = cfg_for(design, (1 << log2) if design != "chaining" else 7 * (1 << log2), seed=12)
+    t = _table(cfg, multi_stream=True)
+    o = _oracle(cfg)
+    base = _keys(31, int(t.capacity_slots * 0.5))
+    third = len(base) // 3
+    stay, gone, hot = base[:third], base[third:2 * third], base[2 * third:]
+    t.upsert_batch(_cuda(base), _cuda(base & np.uint64(0xFFFF)))
+    o.upsert_batch(base, base & np.uint64(0xFFFF))
+    fresh = _keys(32, int(t.capacity_slots * 0.2))
+    add_a = np.concatenate([hot, fresh[: len(fresh) // 2]])
+    add_b = np.concatenate([hot[::2], fresh[len(fresh) // 4:]])
+    va = np.full(len(add_a), 3, dtype=np.uint64)
+    vb = np.full(len(add_b), 5, dtype=np.uint64)
+    ka, kb, kg, ks = _cuda(add_a), _cuda(add_b), _cuda(gone), _cuda(stay)
+    dva, dvb = _cuda(va), _cuda(vb)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    out = {}
+    with torch.cuda.stream(streams[0]):
+        out["a"] = t.upsert_batch(ka, dva, merge="add", check=False)
+    with torch.cuda.stream(streams[1]):
+        out["b"] = t.upsert_batch(kb, dvb, merge="add", check=False)
+    with torch.cuda.stream(streams[2]):
+        out["e"] = t.erase_batch(kg, check=False)
+    with torch.cuda.stream(streams[3]):
+        out["q"] = t.query_batch(ks, check=False)
+    torch.cuda.synchronize()
+    o.upsert_batch(add_a, va, "add")
+    o.upsert_batch(add_b, vb, "add")
+    o.erase_batch(gone)
+    assert not (_np(out["a"]) == 2).any() and not (_np(out["b"]) == 2).any()
+    assert bool(out["e"].all())
+    f, v = out["q"]
+    assert bool(f.all())
+    np.testing.assert_array_equal(_np(v), stay & np.uint64(0xFFFF))
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
