@@ -327,7 +327,7 @@ def run_ours(args, rank, world):
     qry_bytes = (QUERY_TABLE_B + QUERY_IO_B) * n
     ins_gbs = ins_bytes / (ms_ins / 1000) / 1e9
     qry_gbs = qry_bytes / (ms_qry / 1000) / 1e9
-    traffic = None
+    traffic = qtraffic = None
     ceiling = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -335,6 +335,7 @@ def run_ours(args, rank, world):
             pj = json.load(open(prof))
             if pj.get("log2_slots") == args.log2_slots and pj.get("design") == args.design:
                 traffic = pj.get("insert_dram_bytes_per_launch")
+                qtraffic = pj.get("query_dram_bytes_per_launch")
             ceiling = pj.get("random_request_ceiling_g_per_s")
         except Exception:  # noqa: BLE001
             traffic = None
@@ -372,7 +373,8 @@ def run_ours(args, rank, world):
             "algorithmic_bytes_per_op": INSERT_TABLE_B + INSERT_IO_B,
             "query_kernel": {"kernel": "k_query_p2md_coop", "achieved": round(qry_gbs, 1),
                              "frac": round(qry_gbs / peak, 4),
-                             "algorithmic_bytes_per_op": QUERY_TABLE_B + QUERY_IO_B},
+                             "algorithmic_bytes_per_op": QUERY_TABLE_B + QUERY_IO_B,
+                             "traffic": qtraffic},
             "random_access": {
                 "unit": "G random DRAM line accesses/s (reads + write-backs)",
                 "ceiling": ceiling,
