@@ -341,6 +341,42 @@ def test_p2md_2pow28_fill_and_query_properties():
     assert t.duplicate_count() == 0
 
 
+def test_p2md_2pow30_north_star_size_properties():
+    """The north-star size: 2^30 slots (18 GiB of table), 966,367,641 inserts
+    to 0.9 in one batch, then every key queried plus 2^24 absent keys --
+    statuses, occupied count and checksum equal to numpy's over the inputs,
+    every value found, no absent key found, no duplicates."""
+    from paper_2509_16407_b200.core import TableConfig
+    from paper_2509_16407_b200.workload import mix64_np
+    cap = 1 << 30
+    free, _total = torch.cuda.mem_get_info()
+    if free < 48 << 30:
+        pytest.skip("needs ~48 GiB of free device memory")
+    t = _table(TableConfig(design="p2_md", capacity_slots=cap, seed=42))
+    n = int(cap * 0.9)
+    keys = _keys(4242, n)
+    dk = _cuda(keys)
+    dv = _cuda(keys >> np.uint64(7))
+    st = _np(t.upsert_batch(dk, dv))
+    full = st == 2
+    assert int(full.sum()) <= 3 and not (st == 1).any() and not (st > 2).any()
+    ins = ~full
+    with np.errstate(over="ignore"):
+        ki, vi = keys[ins], keys[ins] >> np.uint64(7)
+        want = (int(ins.sum()), int(ki.sum(dtype=np.uint64)), int(vi.sum(dtype=np.uint64)),
+                int(np.bitwise_xor.reduce(mix64_np(ki ^ mix64_np(vi)))))
+    del ki, vi
+    assert t.checksum() == want
+    found, got = t.query_batch(dk)
+    np.testing.assert_array_equal(_np(found).astype(bool), ins)
+    m = torch.from_numpy(ins).cuda()
+    assert torch.equal(got.view(torch.int64)[m], dv.view(torch.int64)[m])
+    del found, got, m
+    f2, _ = t.query_batch(_cuda(_keys(4343, 1 << 24)))
+    assert int(f2.sum()) == 0
+    assert t.duplicate_count() == 0
+
+
 # ----------------------------------------------------- sharding kernels
 
 @pytest.mark.parametrize("log2", [0, 1, 3, 6])
