@@ -35,12 +35,13 @@
 // a balanced half-full table and the simulation shows 0 FULL (6 fills at
 // 2^28, 8 at 2^26), as for random order.
 // Phase B is the ordinary locked kernel (k_upsert_p2md_rounds) over the
-// compacted deferred ops, so alternate-bucket routing, FULL handling and
-// statuses are exactly those of the per-op path.  It visits the deferred
-// records in a pseudo-random order (feistel_perm, ws_fast.cuh): processed in
-// partition (bucket) order, the least-loaded choices of early buckets starve
-// late ones and a 0.9 fill reports FULLs that no random order produces
-// (oracle-checked: bucket order 5 FULL at 2^16 slots, 33 at 2^20; random 0).
+// deferred ops (a bit per batch index), so alternate-bucket routing, FULL
+// handling and statuses are exactly those of the per-op path.  It visits them
+// in BATCH order, like a plain per-op launch: processed in partition (bucket)
+// order, the least-loaded choices of early buckets starve late ones and a
+// 0.9 fill reports FULLs that no random order produces (oracle-checked:
+// bucket order 5 FULL at 2^16 slots, 33 at 2^20; random 0), and any
+// structured order (group order, a Weyl stride) measurably does the same.
 //
 // Ownership instead of locks: phase A takes no bucket locks because each
 // bucket is touched by exactly one CTA (the owner of its group); the path is
@@ -301,7 +302,6 @@ struct ApplySmem {
   u32 lbt[ACAP];        // local bucket << 16 | tag
   u16 rank[ACAP];
   u16 order[ACAP];      // bucket-sorted op positions
-  u16 defer[ACAP];      // deferred op positions
   u16 whist[AW][GBMAX];
   u32 btot[GBMAX];
   u32 bstart[GBMAX];
@@ -312,8 +312,7 @@ struct ApplySmem {
   u64 wk[AW][32];       // warp path: slot keys / values of the bucket
   u64 wv[AW][32];
   u64 fv[AW][32];       // warp path: op values (same-key folding)
-  u32 ndefer, nslow;
-  u64 dbase;
+  u32 nslow;
 };
 
 // The chunk list: group g's ops [goff[g], goff[g+1]) split into ACAP pieces.
@@ -338,7 +337,7 @@ __device__ __forceinline__ void apply_prefetch(ABuf& B, const Dev& d, const u64*
 // warp path for one bucket: ops order[bs0 .. bs0+cnt), exact serial semantics
 __device__ void apply_bucket_warp(ApplySmem& S, ABuf& B, const u64* bk, const u64* bv, const u32* bi,
                                   const Dev& d, u64 b, u32 lb, u32 bs0, u32 cnt, bool te, int cap, int merge,
-                                  u8* status) {
+                                  u8* status, u32* dmask) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const u32 lane_lt = (1u << lane) - 1;
   u16* bt = B.tags + lb * 32;
@@ -408,7 +407,7 @@ __device__ void apply_bucket_warp(ApplySmem& S, ABuf& B, const u64* bk, const u6
     if (ins) newm |= ((ins == 32 ? 0xFFFFFFFFu : ((1u << ins) - 1)) << used);
     used += ins;
     if (act && status && (found || (lslot >= 0 && !isl))) status[bi[p]] = S_UPDATED;
-    if (act && !found && lslot < 0) S.defer[atomicAdd(&S.ndefer, 1u)] = (u16)p;
+    if (act && !found && lslot < 0) atomicOr(dmask + (bi[p] >> 5), 1u << (bi[p] & 31));
     __syncwarp();
   }
   if (dirty) {
@@ -420,8 +419,8 @@ __device__ void apply_bucket_warp(ApplySmem& S, ABuf& B, const u64* bk, const u6
 
 __global__ void __launch_bounds__(AT, 1) k_bulk_apply(Dev d, const u64* __restrict__ K, const u64* __restrict__ V,
                                                       const u32* __restrict__ I, const u32* __restrict__ goff, u64 G,
-                                                      int gb_log2, int cap, int merge, u8* status, BulkRec* DR,
-                                                      u64* dcount, int gated) {
+                                                      int gb_log2, int cap, int merge, u8* status, u32* dmask,
+                                                      int gated) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
   if (blockIdx.x >= G) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -460,7 +459,7 @@ __global__ void __launch_bounds__(AT, 1) k_bulk_apply(Dev d, const u64* __restri
     for (u32 x = lane; x < GBMAX; x += 32) S.whist[w][x] = 0;
     for (u32 q = tid; q < HCAP / 4; q += AT) reinterpret_cast<uint4*>(S.hkey)[q] = make_uint4(0, 0, 0, 0);
     for (u32 x = tid; x < GBMAX; x += AT) { S.bflag[x] = 0; S.wback[x] = 0; }
-    if (tid == 0) { S.ndefer = 0; S.nslow = 0; }
+    if (tid == 0) S.nslow = 0;
     cp_async_wait<1>();
     __syncthreads();
     for (u32 p = tid; p < m; p += AT) {
@@ -556,7 +555,7 @@ __global__ void __launch_bounds__(AT, 1) k_bulk_apply(Dev d, const u64* __restri
         const u32 last = min(u0 + S.btot[lb], (u32)cap) - 1;
         if (slot == last && !(slot & 1)) st_cell(d.cells + 2 * (b * 32 + slot + 1), 0, 0);
       } else {
-        S.defer[atomicAdd(&S.ndefer, 1u)] = (u16)p;
+        atomicOr(dmask + (bi[p] >> 5), 1u << (bi[p] & 31));  // phase B runs it
       }
     }
     for (u32 x = tid; x < nbk; x += AT) {
@@ -570,24 +569,14 @@ __global__ void __launch_bounds__(AT, 1) k_bulk_apply(Dev d, const u64* __restri
     // --- warp path for buckets with key collisions
     for (u32 e = w; e < S.nslow; e += AW) {
       const u32 lb = S.slow[e];
-      apply_bucket_warp(S, B, bk, bv, bi, d, b_lo + lb, lb, S.bstart[lb], S.btot[lb], te, cap, merge, status);
+      apply_bucket_warp(S, B, bk, bv, bi, d, b_lo + lb, lb, S.bstart[lb], S.btot[lb], te, cap, merge, status,
+                        dmask);
     }
     __syncthreads();
     // --- tag blocks of buckets that claimed slots; deferred ops
     for (u32 q = tid; q < nbk * 16; q += AT) {
       if (S.wback[q >> 4])
         st_u32_relaxed(reinterpret_cast<u32*>(d.tags + b_lo * 32) + q, reinterpret_cast<const u32*>(B.tags)[q]);
-    }
-    const u32 nd = S.ndefer;
-    if (nd) {
-      if (tid == 0) S.dbase = atomicAdd((unsigned long long*)dcount, (unsigned long long)nd);
-      __syncthreads();
-      for (u32 q = tid; q < nd; q += AT) {
-        const u32 p = S.defer[q];
-        ulonglong2* r = reinterpret_cast<ulonglong2*>(DR + S.dbase + q);
-        __stcg(r, make_ulonglong2(bk[p], bv[p]));
-        __stcg(r + 1, make_ulonglong2((u64)bi[p], 0ull));
-      }
     }
     if (!have_next) break;
     // the rest of a group continues from this chunk's (updated) tag blocks
@@ -703,12 +692,13 @@ cudaError_t bulk_upsert_p2md(const Dev& d, const u64* keys, const u64* vals, u64
   const GroupFn gf{d.nbm, d.seeds[0], plan.gb_log2};
 
   // scratch: two (key, value, index) buffers, digit histograms, group
-  // offsets, deferred-op records (one 32-byte sector each)
-  u64 *K0 = nullptr, *V0 = nullptr, *K1 = nullptr, *V1 = nullptr, *dcount = nullptr;
+  // offsets, the deferral bitmap (one bit per batch op)
+  u64 *K0 = nullptr, *V0 = nullptr, *K1 = nullptr, *V1 = nullptr;
   u32 *I0 = nullptr, *I1 = nullptr, *counts = nullptr, *offs = nullptr, *gcnt = nullptr, *goff = nullptr;
-  BulkRec* DR = nullptr;
+  u32* dmask = nullptr;
   void* tmp = nullptr;
   const u64 G = plan.groups;
+  const u64 mwords = (n + 31) / 32;
   size_t tb1 = 0, tb2 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb1, counts, offs, (int64_t)(NB * C), s);
   cub::DeviceScan::ExclusiveSum(nullptr, tb2, gcnt, goff, (int64_t)(G + 1), s);
@@ -718,15 +708,14 @@ cudaError_t bulk_upsert_p2md(const Dev& d, const u64* keys, const u64* vals, u64
   WS_BULK_CK(cudaMallocAsync((void**)&K1, 8 * n, s));
   WS_BULK_CK(cudaMallocAsync((void**)&V1, 8 * n, s));
   WS_BULK_CK(cudaMallocAsync((void**)&I1, 4 * n, s));
-  WS_BULK_CK(cudaMallocAsync((void**)&DR, sizeof(BulkRec) * n, s));
+  WS_BULK_CK(cudaMallocAsync((void**)&dmask, 4 * mwords, s));
   WS_BULK_CK(cudaMallocAsync((void**)&counts, 4 * NB * C, s));
   WS_BULK_CK(cudaMallocAsync((void**)&offs, 4 * NB * C, s));
   WS_BULK_CK(cudaMallocAsync((void**)&gcnt, 4 * (G + 1), s));
   WS_BULK_CK(cudaMallocAsync((void**)&goff, 4 * (G + 1), s));
-  WS_BULK_CK(cudaMallocAsync((void**)&dcount, 16, s));
   WS_BULK_CK(cudaMallocAsync(&tmp, std::max(tb1, tb2) + 16, s));
   WS_BULK_CK(cudaMemsetAsync(gcnt, 0, 4 * (G + 1), s));
-  WS_BULK_CK(cudaMemsetAsync(dcount, 0, 16, s));
+  WS_BULK_CK(cudaMemsetAsync(dmask, 0, 4 * mwords, s));
   if (status) WS_BULK_CK(cudaMemsetAsync(status, S_INSERTED, n, s));
 
   const u64* ik = keys;
@@ -752,19 +741,19 @@ cudaError_t bulk_upsert_p2md(const Dev& d, const u64* keys, const u64* vals, u64
   apply_attr();
   const u64 gA = std::min<u64>(G, (u64)sms);
   k_bulk_apply<<<(unsigned)gA, AT, sizeof(ApplySmem), s>>>(d, ik, iv, ii, goff, G, plan.gb_log2,
-                                                            std::min(plan.cap, d.shortcut), merge, status, DR,
-                                                            dcount, gated);
+                                                            std::min(plan.cap, d.shortcut), merge, status, dmask,
+                                                            gated);
   WS_BULK_CK(cudaGetLastError());
   if (!plan.skip_b) {
-    // phase B: the locked per-op kernel over the deferred ops, permuted
+    // phase B: the locked per-op kernel over the deferred ops, in batch order
     u64 gB = (n + 255) / 256;
     gB = std::min<u64>(gB, (u64)sms * 8);
     gB = std::min<u64>(gB, std::max<u64>((d.nb + 255) / 256, 4));
-    bulk_phase_b(d, DR, n, merge, status, gated, dcount, (unsigned)std::max<u64>(gB, 1), s);
+    bulk_phase_b(d, keys, vals, n, merge, status, gated, dmask, (unsigned)std::max<u64>(gB, 1), s);
     WS_BULK_CK(cudaGetLastError());
   }
   for (void* p : {(void*)K0, (void*)V0, (void*)I0, (void*)K1, (void*)V1, (void*)I1, (void*)counts, (void*)offs,
-                  (void*)gcnt, (void*)goff, (void*)dcount, tmp, (void*)DR})
+                  (void*)gcnt, (void*)goff, tmp, (void*)dmask})
     cudaFreeAsync(p, s);
   return cudaSuccess;
 }

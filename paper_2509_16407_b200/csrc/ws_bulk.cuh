@@ -27,16 +27,11 @@ cudaError_t bulk_upsert_p2md(const Dev& d, const u64* keys, const u64* vals, u64
 
 void bulk_preload();
 
-// Deferred op record: one 32-byte sector (phase B reads it at a random position).
-struct BulkRec {
-  u64 key, val, idx, pad;
-};
-
 // Phase B launcher (defined beside the rounds kernel in ws_d_p2_md.cu): the
-// locked per-op upsert over the n_dev[0] deferred records, walked in a stride
-// permutation, statuses other than INSERTED scattered to status[rec.idx].
-void bulk_phase_b(const Dev& d, const BulkRec* recs, u64 n_max, int merge, u8* status, int gated,
-                  const u64* n_dev, unsigned grid, cudaStream_t s);
+// locked per-op upsert over the batch ops whose bit is set in dmask (one bit
+// per batch index), in batch order; statuses written at those indices.
+void bulk_phase_b(const Dev& d, const u64* keys, const u64* vals, u64 n, int merge, u8* status, int gated,
+                  const u32* dmask, unsigned grid, cudaStream_t s);
 
 // 16-byte aligned key / value arrays (the cp.async staging needs them)
 bool bulk_aligned(const void* keys, const void* vals);

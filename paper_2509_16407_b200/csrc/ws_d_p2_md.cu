@@ -108,10 +108,10 @@ static void p2_md_preload(bool def) {
   preload_fn(k_upsert_p2md_rounds<true, 1, true>);
   bulk_preload();
 }
-void bulk_phase_b(const Dev& d, const BulkRec* recs, u64 n_max, int merge, u8* status, int gated,
-                  const u64* n_dev, unsigned grid, cudaStream_t s) {
-  k_upsert_p2md_rounds<true, 1, false, true, true><<<grid, 256, 0, s>>>(
-      d, nullptr, nullptr, n_max, merge, status, 0, gated, reinterpret_cast<const u64*>(recs), n_dev);
+void bulk_phase_b(const Dev& d, const u64* keys, const u64* vals, u64 n, int merge, u8* status, int gated,
+                  const u32* dmask, unsigned grid, cudaStream_t s) {
+  k_upsert_p2md_rounds<true, 1, false, true, true><<<grid, 256, 0, s>>>(d, keys, vals, n, merge, status, 0, gated,
+                                                                        dmask);
 }
 
 Launchers launchers_p2_md() { return Launchers{p2_md_ops, p2_md_query, p2_md_locate, p2_md_preload}; }

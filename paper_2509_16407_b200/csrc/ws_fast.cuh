@@ -372,30 +372,6 @@ __global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __re
   }
 }
 
-// Pseudo-random bijection of [0, n): a 4-round balanced Feistel network on
-// `bits` (even, 2^bits >= n) bits keyed by `key`, cycle-walked back into
-// range (expected < 4 steps).  Bulk phase B visits its deferred records in
-// this order: the records are bucket-sorted, and any structured visiting
-// order (bucket order, group order, even a golden-ratio Weyl stride once
-// ~10^5 ops run concurrently) leaves measurable FULLs in a 0.9 fill that a
-// random order does not.
-__device__ __forceinline__ u64 feistel_perm(u64 x, u64 n, int bits, u64 key) {
-  const int h = bits >> 1;
-  const u64 m = (1ull << h) - 1;
-  do {
-    u64 l = x >> h, r = x & m;
-#pragma unroll
-    for (int rd = 0; rd < 4; rd++) {
-      const u64 f = mix64(r ^ (key + (u64)rd * 0x9E3779B97F4A7C15ull)) & m;
-      const u64 t = l ^ f;
-      l = r;
-      r = t;
-    }
-    x = (l << h) | r;
-  } while (x >= n);
-  return x;
-}
-
 // =============================================== warp-synchronous rounds
 //
 // P2-MD upsert, one thread per op, in warp-synchronous lock rounds.  A
@@ -529,43 +505,61 @@ __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64*
 // under the bucket lock; storing (0,0) there too makes the 32-byte sector
 // fully valid in L2, so its eviction needs no ECC read-modify-write of the
 // untouched half (measured ~1 DRAM sector per insert without it).
-template <bool F64, int MINB, bool PHASED, bool FILL = false, bool REC = false>
+template <bool F64, int MINB, bool PHASED, bool FILL = false, bool MASK = false>
 __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, int merge,
                                                             u8* status, int conc_erase, int gated,
-                                                            const u64* __restrict__ recs = nullptr,
-                                                            const u64* n_dev = nullptr) {
+                                                            const u32* __restrict__ dmask = nullptr) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
-  // bulk phase B (ws_bulk.cu): ops are 32-byte records (key, value, batch
-  // index, pad) counted on the device (n_dev[0]) and visited in a
-  // pseudo-random order (feistel_perm), statuses other than INSERTED
-  // (pre-filled) scattered to the batch index
-  if constexpr (REC) n = *n_dev;
+  // bulk phase B (ws_bulk.cu): only the batch ops whose bit is set in dmask
+  // (deferred by phase A) run; the rest already took effect.  Each warp
+  // walks a contiguous range of bitmap words and packs up to 32 deferred ops
+  // (whole words) into its lanes per pass, so lanes stay busy at ~30% density;
+  // the visiting order is batch order within each warp's range, as for the
+  // full per-op launch.
   const u32 te0 = ld_u32_relaxed(d.state);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const u64 c0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
-  int pbits = 0;
-  if constexpr (REC) {
-    while ((1ull << pbits) < n) pbits++;
-    pbits += pbits & 1;
+  __shared__ u64 mpos[MASK ? 8 : 1][32];
+  u64 cw = 0, whi = 0;
+  if constexpr (MASK) {
+    const u64 mwords = (n + 31) / 32, per = (mwords + nwarps - 1) / nwarps;
+    cw = c0 * per;
+    whi = cw + per < mwords ? cw + per : mwords;
   }
-  for (u64 c = c0; c * 32 < n; c += nwarps) {
-    const u64 i = c * 32 + lane;
+  for (u64 c = c0; MASK ? cw < whi : c * 32 < n; c += nwarps) {
+    u64 i = c * 32 + lane;
     bool pending = i < n;
-    u64 key = 0, val = 0, b0 = 0, b1 = 0, sidx = 0;
+    if constexpr (MASK) {
+      const u64 wi = cw + lane;
+      const u32 bits = wi < whi ? __ldg(dmask + wi) : 0u;
+      const u32 cnt = __popc(bits);
+      u32 incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int k = __popc(__ballot_sync(0xFFFFFFFFu, incl <= 32));  // whole words, <= 32 ops
+      const u32 total = __shfl_sync(0xFFFFFFFFu, incl, k - 1);
+      u64* mp = mpos[(threadIdx.x >> 5) & 7];
+      if (lane < k) {
+        u32 o = incl - cnt;
+        for (u32 b = bits; b; b &= b - 1) mp[o++] = wi * 32 + (__ffs(b) - 1);
+      }
+      __syncwarp();
+      pending = (u32)lane < total;
+      i = pending ? mp[lane] : 0;
+      __syncwarp();
+      cw += k;
+    }
+    const bool mine = pending;
+    u64 key = 0, val = 0, b0 = 0, b1 = 0;
     u16 tag = 1;
     if (pending) {
-      if constexpr (REC) {
-        const u64 pj = feistel_perm(i, n, pbits, d.seeds[2]);
-        const ulonglong2 r0 = __ldg(reinterpret_cast<const ulonglong2*>(recs + 4 * pj));
-        key = r0.x;
-        val = r0.y;
-        sidx = __ldg(recs + 4 * pj + 2);
-      } else {
-        key = __ldg(keys + i);
-        val = __ldg(vals + i);
-      }
+      key = __ldg(keys + i);
+      val = __ldg(vals + i);
       const u64 h0 = mix64(key ^ d.seeds[0]);
       b0 = d.nbm(h0 >> 16);
       const u16 t = (u16)(h0 & 0xFFFF);
@@ -695,10 +689,7 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
         if (backoff < 4096) backoff <<= 1;
       }
     }
-    if (i < n && status) {
-      if constexpr (!REC) status[i] = st;
-      else if (st != S_INSERTED) status[sidx] = st;
-    }
+    if (status && (MASK ? mine : i < n)) status[i] = st;
   }
 }
 
