@@ -252,14 +252,85 @@ bool bulk_eligible(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n,
   return true;
 }
 
+__global__ void k_comb_iota(u64 n, u32* idx);
+
+// internal flags of run_device_plain
+constexpr u32 kF_VALIDATED = 1u << 30;  // the caller validated the batch; keep the kernels gated
+constexpr u32 kF_NO_KIND_SORT = 1u << 29;
+
+__global__ void k_kind_gather(const u32* __restrict__ perm, const u64* __restrict__ keys,
+                              const u64* __restrict__ vals, u64 n, u64* kp, u64* vp) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
+    const u32 i = perm[j];
+    kp[j] = keys[i];
+    if (vals) vp[j] = vals[i];
+  }
+}
+__global__ void k_kind_scatter(const u32* __restrict__ perm, const u8* __restrict__ sp, const u64* __restrict__ vop,
+                               u64 n, u8* status, u64* vout) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
+    const u32 i = perm[j];
+    if (status) status[i] = sp[j];
+    if (vout) vout[i] = vop[j];
+  }
+}
+
+int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
+                     u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
+                     bool query_only);
+
+// Mixed batches: the generic op kernel carries every op kind's code path
+// (~100 KB of SASS for a 32-slot md design); with kinds interleaved at random
+// every warp walks all of them and the SMs stall on instruction fetch (ncu:
+// 65% "no instruction" stalls in the iceberg aging batch).  Large mixed
+// batches are therefore run in op-kind order -- a stable partition by kind,
+// a gather, the launch, a scatter of the results back -- which is just another
+// serial order of the concurrent batch.
+int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
+                       u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert) {
+  int rc = validate(t, keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags);
+  if (rc) return rc;
+  u8 *op_p = nullptr, *st_p = nullptr;
+  u32 *idx = nullptr, *perm = nullptr;
+  u64 *k_p = nullptr, *v_p = nullptr, *vo_p = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, ops, op_p, idx, perm, (int64_t)n, 0, 4, s);
+  WS_CK(cudaMallocAsync((void**)&op_p, n, s));
+  WS_CK(cudaMallocAsync((void**)&st_p, n, s));
+  WS_CK(cudaMallocAsync((void**)&idx, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&perm, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&k_p, 8 * n, s));
+  if (vals) WS_CK(cudaMallocAsync((void**)&v_p, 8 * n, s));
+  if (vout) WS_CK(cudaMallocAsync((void**)&vo_p, 8 * n, s));
+  WS_CK(cudaMallocAsync(&tmp, tb + 16, s));
+  k_comb_iota<<<grid_for(n), kThreads, 0, s>>>(n, idx);
+  cub::DeviceRadixSort::SortPairs(tmp, tb, ops, op_p, idx, perm, (int64_t)n, 0, 4, s);
+  k_kind_gather<<<grid_for(n), kThreads, 0, s>>>(perm, keys, vals, n, k_p, v_p);
+  rc = cuda_err(cudaGetLastError());
+  const u32 inner = (flags & ~WS_F_SYNC_CHECK) | kF_NO_KIND_SORT |
+                    ((flags & WS_F_NO_CHECK) ? 0u : (kF_VALIDATED | WS_F_NO_CHECK));
+  if (!rc) rc = run_device_plain(t, op_p, uop, k_p, v_p, n, st_p, vo_p, s, inner, has_erase, has_upsert, false);
+  if (!rc) {
+    k_kind_scatter<<<grid_for(n), kThreads, 0, s>>>(perm, st_p, vo_p, n, status, vout);
+    rc = cuda_err(cudaGetLastError());
+  }
+  for (void* p : {(void*)op_p, (void*)st_p, (void*)idx, (void*)perm, (void*)k_p, (void*)v_p, (void*)vo_p, tmp})
+    if (p) cudaFreeAsync(p, s);
+  return rc;
+}
+
 int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                      bool query_only) {
+  if (ops && !query_only && n >= (1u << 16) && n < (1ull << 32) &&
+      !(flags & (WS_F_SERIAL | kF_NO_KIND_SORT)))
+    return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert);
   const bool sync = (flags & WS_F_SYNC_CHECK) != 0;
   int rc = validate(t, keys, ops, n, s, sync, flags);
   if (rc) return rc;
   if (!n) return WS_OK;
-  const int gated = (flags & WS_F_NO_CHECK) ? 0 : 1;
+  const int gated = (flags & kF_VALIDATED) ? 1 : (flags & WS_F_NO_CHECK) ? 0 : 1;
   if (has_erase) t->maybe_tomb = true;
   if (!query_only && !ops && bulk_eligible(t, uop, keys, vals, n, flags, s)) {
     BulkPlan plan = bulk_plan(n, t->d.nb, t->tune_bulk_gb);
