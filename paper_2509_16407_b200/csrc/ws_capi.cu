@@ -279,43 +279,82 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                      bool query_only);
 
+// first index of every op-byte value in the sorted op array (~0 when absent)
+__global__ void k_seg_starts(const u8* __restrict__ op_sorted, u64 n, u64* start) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x)
+    if (j == 0 || op_sorted[j] != op_sorted[j - 1]) start[op_sorted[j]] = j;
+}
+
 // Mixed batches: the generic op kernel carries every op kind's code path
 // (~100 KB of SASS for a 32-slot md design); with kinds interleaved at random
 // every warp walks all of them and the SMs stall on instruction fetch (ncu:
 // 65% "no instruction" stalls in the iceberg aging batch).  Large mixed
-// batches are therefore run in op-kind order -- a stable partition by kind,
-// a gather, the launch, a scatter of the results back -- which is just another
-// serial order of the concurrent batch.
+// batches are therefore stably partitioned by op byte (kind | merge << 4) and
+// each segment runs as its own uniform launch -- upserts of one merge through
+// the design's upsert kernel (the tuned lock-round kernel for P2-MD), erases,
+// queries through the lock-free query kernel -- one after another on the
+// stream, then the results are scattered back.  Running the segments in
+// sequence is one serial order of the concurrent batch.
 int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
                        u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert) {
   int rc = validate(t, keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags);
   if (rc) return rc;
   u8 *op_p = nullptr, *st_p = nullptr;
   u32 *idx = nullptr, *perm = nullptr;
-  u64 *k_p = nullptr, *v_p = nullptr, *vo_p = nullptr;
+  u64 *k_p = nullptr, *v_p = nullptr, *vo_p = nullptr, *starts = nullptr;
   void* tmp = nullptr;
   size_t tb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, ops, op_p, idx, perm, (int64_t)n, 0, 4, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, ops, op_p, idx, perm, (int64_t)n, 0, 8, s);
   WS_CK(cudaMallocAsync((void**)&op_p, n, s));
   WS_CK(cudaMallocAsync((void**)&st_p, n, s));
   WS_CK(cudaMallocAsync((void**)&idx, 4 * n, s));
   WS_CK(cudaMallocAsync((void**)&perm, 4 * n, s));
   WS_CK(cudaMallocAsync((void**)&k_p, 8 * n, s));
+  WS_CK(cudaMallocAsync((void**)&starts, 8 * 256, s));
   if (vals) WS_CK(cudaMallocAsync((void**)&v_p, 8 * n, s));
   if (vout) WS_CK(cudaMallocAsync((void**)&vo_p, 8 * n, s));
   WS_CK(cudaMallocAsync(&tmp, tb + 16, s));
   k_comb_iota<<<grid_for(n), kThreads, 0, s>>>(n, idx);
-  cub::DeviceRadixSort::SortPairs(tmp, tb, ops, op_p, idx, perm, (int64_t)n, 0, 4, s);
+  cub::DeviceRadixSort::SortPairs(tmp, tb, ops, op_p, idx, perm, (int64_t)n, 0, 8, s);
   k_kind_gather<<<grid_for(n), kThreads, 0, s>>>(perm, keys, vals, n, k_p, v_p);
+  WS_CK(cudaMemsetAsync(starts, 0xFF, 8 * 256, s));
+  k_seg_starts<<<grid_for(n), kThreads, 0, s>>>(op_p, n, starts);
   rc = cuda_err(cudaGetLastError());
-  const u32 inner = (flags & ~WS_F_SYNC_CHECK) | kF_NO_KIND_SORT |
+  std::vector<u64> st_h(256);
+  if (!rc) rc = cuda_err(cudaMemcpyAsync(st_h.data(), starts, 8 * 256, cudaMemcpyDeviceToHost, s));
+  if (!rc) rc = cuda_err(cudaStreamSynchronize(s));
+  const u32 inner = (flags & ~(WS_F_SYNC_CHECK | WS_F_COMBINE)) | kF_NO_KIND_SORT |
                     ((flags & WS_F_NO_CHECK) ? 0u : (kF_VALIDATED | WS_F_NO_CHECK));
-  if (!rc) rc = run_device_plain(t, op_p, uop, k_p, v_p, n, st_p, vo_p, s, inner, has_erase, has_upsert, false);
+  // segments in op-byte order
+  std::vector<std::pair<u64, int>> seg;
+  for (int v = 0; v < 256; v++)
+    if (st_h[v] != ~0ull) seg.push_back({st_h[v], v});
+  std::sort(seg.begin(), seg.end());
+  for (size_t q = 0; q < seg.size() && !rc; q++) {
+    const u64 lo = seg[q].first, hi = q + 1 < seg.size() ? seg[q + 1].first : n;
+    const u8 v = (u8)seg[q].second;
+    const int kind = v & 15, merge = v >> 4;
+    const u64 m = hi - lo;
+    if (kind == OP_UPSERT && merge <= M_MIN && v_p) {
+      rc = run_device_plain(t, nullptr, v, k_p + lo, v_p + lo, m, st_p + lo, nullptr, s, inner, false, true, false);
+      if (vo_p && !rc) rc = cuda_err(cudaMemsetAsync(vo_p + lo, 0, 8 * m, s));
+    } else if (kind == OP_ERASE && merge == 0) {
+      rc = run_device_plain(t, nullptr, v, k_p + lo, nullptr, m, st_p + lo, nullptr, s, inner, true, false, false);
+      if (vo_p && !rc) rc = cuda_err(cudaMemsetAsync(vo_p + lo, 0, 8 * m, s));
+    } else if (kind == OP_QUERY && merge == 0) {
+      rc = run_device_plain(t, nullptr, v, k_p + lo, nullptr, m, st_p + lo, vo_p ? vo_p + lo : nullptr, s, inner,
+                            false, false, true);
+    } else {  // value-less upserts or invalid op bytes (gated): the generic kernel handles them
+      rc = run_device_plain(t, op_p + lo, 0, k_p + lo, v_p ? v_p + lo : nullptr, m, st_p + lo,
+                            vo_p ? vo_p + lo : nullptr, s, inner, has_erase, has_upsert, false);
+    }
+  }
   if (!rc) {
     k_kind_scatter<<<grid_for(n), kThreads, 0, s>>>(perm, st_p, vo_p, n, status, vout);
     rc = cuda_err(cudaGetLastError());
   }
-  for (void* p : {(void*)op_p, (void*)st_p, (void*)idx, (void*)perm, (void*)k_p, (void*)v_p, (void*)vo_p, tmp})
+  for (void* p : {(void*)op_p, (void*)st_p, (void*)idx, (void*)perm, (void*)k_p, (void*)v_p, (void*)vo_p,
+                  (void*)starts, tmp})
     if (p) cudaFreeAsync(p, s);
   return rc;
 }
