@@ -297,7 +297,7 @@ __device__ __forceinline__ bool pair_lock_extra(const Dev& d, const Pair& p, u64
   return p.from_lead(ok) != 0;
 }
 
-__global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __restrict__ keys,
+static __global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __restrict__ keys,
                                                           const u64* __restrict__ vals, u64 n, int merge,
                                                           u8* status, int conc_erase, int gated) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
