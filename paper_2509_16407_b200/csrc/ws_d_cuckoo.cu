@@ -1,5 +1,5 @@
 // Kernel instantiations for the cuckoo design (see ws_kernels.cuh), plus the
-// tuned lock-round query for the default 8-slot buckets.
+// tuned lock-round query and upsert fast path for the default 8-slot buckets.
 #include "ws_kernels.cuh"
 
 #include <algorithm>
@@ -90,7 +90,112 @@ __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* _
   }
 }
 
+// Cuckoo upsert fast path (reference cuckoo.py:68-97, the part before the
+// eviction search): same lock rounds as the query; with all of the key's
+// bucket locks held, scan the buckets in hash order -- a match is merged, else
+// the first bucket with a reusable cell (first TOMB / EMPTY before the
+// bucket's first EMPTY) receives the key.  Ops whose buckets are all full
+// are marked S_RETRY and left to the generic kernel (BFS eviction chains),
+// launched right after on the same stream: one serial order of the batch.
+__global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* __restrict__ keys,
+                                                              const u64* __restrict__ vals, u64 n, int merge,
+                                                              u8* st_out, int gated) {
+  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  const int lane = threadIdx.x & 31;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  const bool locked = !d.phased;
+  for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c * 32 < n; c += nwarps) {
+    const u64 i = c * 32 + lane;
+    bool pending = i < n;
+    const u64 key = pending ? __ldg(keys + i) : 0;
+    const u64 val = pending ? __ldg(vals + i) : 0;
+    u64 uq[8], srt[8];
+    int nu = 0;
+    if (pending) {
+      for (int w = 0; w < d.ways; w++) {
+        const u64 b = d.nbm(mix64(key ^ d.seeds[w]) >> 16);
+        bool dup = false;
+        for (int j = 0; j < nu; j++) dup |= uq[j] == b;
+        if (!dup) uq[nu++] = b;
+      }
+      for (int j = 0; j < nu; j++) srt[j] = uq[j];
+      for (int a = 1; a < nu; a++)
+        for (int b = a; b > 0 && srt[b - 1] > srt[b]; b--) { const u64 t = srt[b]; srt[b] = srt[b - 1]; srt[b - 1] = t; }
+    }
+    int held = 0;
+    u8 st = S_RETRY;
+    unsigned backoff = 64;
+    while (__any_sync(0xFFFFFFFFu, pending)) {
+      if (pending && locked)
+        while (held < nu && try_lock_bucket(d.locks, srt[held])) held++;
+      const bool ready = pending && (!locked || held == nu);
+      if (ready) {
+        i64 hit = -1, free_at = -1;
+        u64 old = 0;
+        for (int q = 0; q < nu && hit < 0; q++) {
+          const u64 lo = uq[q] * 8;
+          i64 fr = -1;
+          bool empty = false;
+#pragma unroll
+          for (int h = 0; h < 4; h++) {
+            if (empty || hit >= 0) break;
+            u64 k[2], v[2];
+            ld_cells2(d.cells + 2 * (lo + 2 * h), k[0], v[0], k[1], v[1]);
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+              if (empty || hit >= 0) break;
+              const u64 slot = lo + 2 * h + e;
+              if (k[e] == key) { hit = (i64)slot; old = v[e]; }
+              else if (k[e] == EMPTY) { if (fr < 0) fr = (i64)slot; empty = true; }
+              else if (k[e] == TOMB) { if (fr < 0) fr = (i64)slot; }
+            }
+          }
+          if (free_at < 0 && fr >= 0) free_at = fr;
+        }
+        if (hit >= 0) {
+          st_cell(d.cells + 2 * (u64)hit, key, apply_merge(merge, old, val));
+          st = S_UPDATED;
+        } else if (free_at >= 0 && publish_cell(d.cells + 2 * (u64)free_at, key, val)) {
+          st = S_INSERTED;
+        }  // else S_RETRY: every bucket full (eviction chain) -> generic kernel
+        pending = false;
+      }
+      if (locked) {
+        __syncwarp();
+        fence_acq_rel();
+        if (ready) {
+          for (int q = 0; q < nu; q++)
+            asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(d.locks + (srt[q] >> 5)),
+                         "r"(~(1u << (srt[q] & 31))) : "memory");
+        }
+      }
+      if (pending) {
+        __nanosleep(backoff + 8 * lane);
+        if (backoff < 4096) backoff <<= 1;
+      }
+    }
+    if (i < n) st_out[i] = st;
+  }
+}
+
 static void cuckoo_ops(const OpsArgs& a, bool def) {
+  const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
+  if (def && upsert_only && !a.instr && !a.serial && !a.redo && a.d.ways <= 8 && a.d.tune_upsert == 4) {
+    u8* st = a.status;
+    if (!st && cudaMallocAsync((void**)&st, a.n, a.s) != cudaSuccess) st = nullptr;
+    if (st) {
+      u64 g = (a.n + 255) / 256;
+      const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
+      g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
+      k_upsert_cuckoo_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, st, a.gated);
+      OpsArgs lo = a;
+      lo.status = st;
+      lo.redo = st;  // the generic kernel runs only the S_RETRY ops (eviction chains)
+      launch_ops_t<D_CUCKOO, 8>(lo);
+      if (st != a.status) cudaFreeAsync(st, a.s);
+      return;
+    }
+  }
   if (def) launch_ops_t<D_CUCKOO, 8>(a); else launch_ops_t<D_CUCKOO, 0>(a);
 }
 static void cuckoo_query(const QueryArgs& a, bool def) {
@@ -109,6 +214,7 @@ static void cuckoo_preload(bool def) {
   if (!def) { preload_t<D_CUCKOO, 0>(); return; }
   preload_t<D_CUCKOO, 8>();
   preload_fn(k_query_cuckoo_rounds);
+  preload_fn(k_upsert_cuckoo_rounds);
 }
 Launchers launchers_cuckoo() { return Launchers{cuckoo_ops, cuckoo_query, cuckoo_locate, cuckoo_preload}; }
 

@@ -14,8 +14,22 @@ n = int(cap * 0.9)
 keys = gen_uniform_keys(42, n)
 t = make_table(TableConfig(design="cuckoo", capacity_slots=cap, seed=42))
 dk = torch.from_numpy(keys.view(np.int64)).cuda().view(torch.uint64)
-st = t.upsert_batch(dk, dk, check=False)
-print("fill statuses", np.bincount(st.cpu().numpy(), minlength=3), flush=True)
+for up in (4, 0, 4):
+    t.tune(upsert=up)
+    t.clear()
+    torch.cuda.synchronize()
+    half = int(cap * 0.5)
+    a, b, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    a.record()
+    s1 = t.upsert_batch(dk[:half], dk[:half], check=False)
+    b.record()
+    s2 = t.upsert_batch(dk[half:], dk[half:], check=False)
+    c2.record()
+    torch.cuda.synchronize()
+    st = torch.cat([s1, s2])
+    print(f"fill upsert={up}: 0->0.5 {a.elapsed_time(b):.2f} ms ({half / a.elapsed_time(b) / 1e6:.2f} G/s), "
+          f"0.5->0.9 {b.elapsed_time(c2):.2f} ms ({(n - half) / b.elapsed_time(c2) / 1e6:.2f} G/s) "
+          f"statuses {np.bincount(st.cpu().numpy(), minlength=3)} checksum {t.checksum()[:2]}", flush=True)
 miss = gen_uniform_keys(derive_seed(42, 0xFEED), n // 2)
 q = np.concatenate([keys[: n // 2], miss])
 np.random.default_rng(1).shuffle(q)
