@@ -82,6 +82,8 @@ enum { WS_OP_UPSERT = 0, WS_OP_ERASE = 1, WS_OP_QUERY = 2 };
                                exactly the reference's sequential semantics */
 #define WS_F_COMBINE 8u     /* fold same-key upserts of the batch before applying them
                                (hot-key / Zipf batches); statuses as if applied in some order */
+#define WS_F_INTERLEAVED 16u /* mixed batch: keep every op kind in ONE interleaved launch (race tests);
+                               default: large mixed batches run as per-kind segments */
 
 /* All derived integers are computed by the host layer exactly as the
  * reference computes them (core.py:209-211, openaddr.py:45-47,351-352,505-507). */

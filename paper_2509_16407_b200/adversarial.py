@@ -124,7 +124,7 @@ def run_adversarial(design: str, buckets: int = 10_000, trials: int = 3, seed: i
         if int((st == 2).sum()):
             raise RuntimeError("adversarial pre-insert hit FULL")
         table.set_delays(profile.max_ns, profile.prob, derive_seed(seed, trial))
-        table.mixed_batch(d_ops, d_keys, d_vals)
+        table.mixed_batch(d_ops, d_keys, d_vals, interleaved=True)  # erase races the inserts
         table.set_delays(0, 0.0, 0)
         dups = table.duplicate_scan()
         assert all(k in y_set for k in dups), "duplicate of a non-replayed key"

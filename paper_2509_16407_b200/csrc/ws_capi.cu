@@ -362,8 +362,8 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
 int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                      bool query_only) {
-  if (ops && !query_only && n >= (1u << 16) && n < (1ull << 32) &&
-      !(flags & (WS_F_SERIAL | kF_NO_KIND_SORT)))
+  if (ops && !query_only && n >= (1u << 16) && n < (1ull << 32) && !t->d.delay_ns &&
+      !(flags & (WS_F_SERIAL | WS_F_INTERLEAVED | kF_NO_KIND_SORT)))
     return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert);
   const bool sync = (flags & WS_F_SYNC_CHECK) != 0;
   int rc = validate(t, keys, ops, n, s, sync, flags);

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256) k_upsert_chain_rounds(Dev d, const u64* _
 
 static void chaining_ops(const OpsArgs& a, bool def) {
   const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
-  if (def && upsert_only && a.status && !a.instr && !a.serial && !a.redo && !a.d.phased && a.d.wpn == 16 &&
+  if (def && upsert_only && a.status && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && !a.d.phased && a.d.wpn == 16 &&
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* 
 
 static void cuckoo_ops(const OpsArgs& a, bool def) {
   const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
-  if (def && upsert_only && !a.instr && !a.serial && !a.redo && a.d.ways <= 8 && a.d.tune_upsert == 4) {
+  if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && a.d.ways <= 8 && a.d.tune_upsert == 4) {
     u8* st = a.status;
     if (!st && cudaMallocAsync((void**)&st, a.n, a.s) != cudaSuccess) st = nullptr;
     if (st) {

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) k_upsert_icemd_rounds(Dev d, const u64* _
 
 static void iceberg_md_ops(const OpsArgs& a, bool def) {
   const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
-  if (def && upsert_only && !a.instr && !a.serial && !a.redo && !a.d.phased && !a.d.lock_elided &&
+  if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && !a.d.phased && !a.d.lock_elided &&
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket

@@ -36,7 +36,7 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
                                                                        a.status, a.conc_erase, a.gated);
     return;
   }
-  if (def && upsert_only && !a.instr && !a.serial && !a.redo && !a.d.lock_elided && a.d.tune_upsert >= 2) {
+  if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && !a.d.lock_elided && a.d.tune_upsert >= 2) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
     g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);

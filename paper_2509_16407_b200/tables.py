@@ -449,10 +449,12 @@ class HashTable:
         self._check(self._lib.ws_erase(self._h, kp, len(k), found.data_ptr(), self._stream(), fl))
         return as_bool(found)
 
-    def mixed_batch(self, ops, keys, values=None, check=True, serial=False, combine=False):
-        """One launch of mixed ops (byte = kind | merge << 4, kind 0 upsert /
-        1 erase / 2 query).  Returns (status uint8, values uint64): upsert
-        status, erase/query found flag, query value."""
+    def mixed_batch(self, ops, keys, values=None, check=True, serial=False, combine=False, interleaved=False):
+        """A concurrent batch of mixed ops (byte = kind | merge << 4, kind 0
+        upsert / 1 erase / 2 query).  Returns (status uint8, values uint64):
+        upsert status, erase/query found flag, query value.  Large batches run
+        as per-kind segment launches; interleaved=True keeps all kinds in one
+        launch (race tests that need erases concurrent with inserts)."""
         torch = _torch()
         o, op, _oc = _as_u8(ops, torch)
         k, kp, kc = _as_u64(keys, torch)
@@ -467,6 +469,8 @@ class HashTable:
             fl |= _native.WS_F_SERIAL
         if combine:
             fl |= _native.WS_F_COMBINE
+        if interleaved:
+            fl |= _native.WS_F_INTERLEAVED
         self._check(self._lib.ws_mixed(self._h, op, kp, vp, len(k), st.data_ptr(), vo.data_ptr(),
                                        self._stream(), fl))
         return st, vo
