@@ -942,24 +942,42 @@ struct Ctx {
     const u64 b = hb(0, key, d.nbm);
     u8 st;
     lock(b);
-    Walk w = ch_walk(key);
-    if (w.m >= 0) {
-      st_cell(node((u64)w.m) + 2 * w.j, key, apply_merge(merge, w.val, val));
-      st = S_UPDATED;
-    } else if (w.fm < 0) {
+    // Phased mode (sync.py:70-102) makes the chain lock a no-op while inserts
+    // of distinct keys into one chain still run concurrently: a free pair is
+    // then claimed by CAS and a new node is linked by CAS on the tail's link
+    // before its first pair is claimed (a loser walks the chain again; an
+    // unlinked node stays EMPTY).  Under the lock plain stores suffice.
+    for (;;) {
+      Walk w = ch_walk(key);
+      if (w.m >= 0) {
+        st_cell(node((u64)w.m) + 2 * w.j, key, apply_merge(merge, w.val, val));
+        st = S_UPDATED;
+        break;
+      }
+      if (w.fm >= 0) {
+        if (!d.phased) {
+          st_cell(node((u64)w.fm) + 2 * w.fj, key, val);
+          st = S_INSERTED;
+          break;
+        }
+        if (publish_cell(node((u64)w.fm) + 2 * w.fj, key, val)) { st = S_INSERTED; break; }
+        continue;
+      }
       const u64 m = atomicAdd(d.chain_next, 1ull);
       if (m >= d.chain_cap) {
         st_u32_relaxed(d.state + 1, 1u);  // host grows the pool and re-runs this op
         st = S_RETRY;
-      } else {
-        touch((u64)d.line_bytes * m);
+        break;
+      }
+      touch((u64)d.line_bytes * m);
+      if (!d.phased) {
         st_cell(node(m), key, val);
         st_u64_release(node(w.tail) + 2 * B(), m);
         st = S_INSERTED;
+        break;
       }
-    } else {
-      st_cell(node((u64)w.fm) + 2 * w.fj, key, val);
-      st = S_INSERTED;
+      if (atomicCAS((unsigned long long*)(node(w.tail) + 2 * B()), 0ull, (unsigned long long)m) != 0ull) continue;
+      if (publish_cell(node(m), key, val)) { st = S_INSERTED; break; }
     }
     unlock(b);
     return st;

@@ -523,3 +523,34 @@ def test_multi_stream_concurrent_launches(design, log2):
     np.testing.assert_array_equal(_np(v), stay & np.uint64(0xFFFF))
     assert dict(t.items()) == o.as_dict()
     assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("design", ["p2_md", "p2", "iceberg_md", "iceberg", "double", "double_md", "cuckoo",
+                                    "chaining"])
+def test_phased_mode_batches_match_oracle(design):
+    """mode="phased" (reference BSP mode, sync.py:70-102: locks are no-ops,
+    one op kind per phase): an insert phase, a query phase, an erase phase
+    and a second insert phase, each one concurrent batch, against the oracle."""
+    cap = 1 << 16
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * 4096, seed=21, mode="phased")
+    t = _table(cfg)
+    o = _oracle(cfg)
+    n = int(t.capacity_slots * (0.8 if design != "chaining" else 1.2))
+    keys = _keys(61, n)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(keys >> np.uint64(3))))
+    ost = o.upsert_batch(keys, keys >> np.uint64(3))
+    assert not (ost != 0).any() and not (st != 0).any()
+    q = np.concatenate([keys[::3], _keys(62, 5000)])
+    f, v = t.query_batch(_cuda(q))
+    of, ov = o.query_batch(q)
+    np.testing.assert_array_equal(_np(f).astype(bool), of)
+    np.testing.assert_array_equal(_np(v), ov)
+    gone = _np(t.erase_batch(_cuda(keys[::4])))
+    ogone = o.erase_batch(keys[::4])
+    np.testing.assert_array_equal(gone.astype(bool), np.asarray(ogone).astype(bool))
+    more = _keys(63, n // 8)
+    st = _np(t.upsert_batch(_cuda(more), _cuda(more)))
+    ost = o.upsert_batch(more, more)
+    np.testing.assert_array_equal(st, ost)
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
