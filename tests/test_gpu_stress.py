@@ -32,7 +32,7 @@ def _np(t):
 
 
 @pytest.mark.parametrize("how", ["mixed", "split", "split_combine"])
-@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "cuckoo", "chaining", "double_md"])
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "cuckoo", "chaining", "double_md", "double"])
 def test_small_table_contention(design, how):
     from paper_2509_16407_b200 import make_table
     from paper_2509_16407_b200.tables import OP_ERASE, OP_QUERY, OP_UPSERT
