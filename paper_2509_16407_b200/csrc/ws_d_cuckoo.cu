@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* 
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
-  const bool locked = !d.phased;
+  const bool locked = true;  // mutations lock even in phased mode (Ctx::ck_lock_all)
   for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c * 32 < n; c += nwarps) {
     const u64 i = c * 32 + lane;
     bool pending = i < n;

@@ -635,17 +635,21 @@ struct Ctx {
     }
     return nu;
   }
-  __device__ void ck_lock_all(const u64* uq, int nu) {  // ascending order: deadlock free
+  // Phased mode (locks are no-ops in the reference, sync.py:70-102) keeps the
+  // locks of cuckoo MUTATIONS: displacement chains move other keys, and two
+  // unlocked movers of one key would both copy it (a duplicate).  Phased
+  // queries stay lock-free (`mut` false).
+  __device__ void ck_lock_all(const u64* uq, int nu, bool mut = true) {  // ascending order: deadlock free
     for (int i = 0; i < nu; i++) touch_lock(uq[i]);
-    if (d.phased) return;
+    if (d.phased && !mut) return;
     u64 s[8];
     for (int i = 0; i < nu; i++) s[i] = uq[i];
     for (int i = 1; i < nu; i++)
       for (int j = i; j > 0 && s[j - 1] > s[j]; j--) { const u64 t = s[j]; s[j] = s[j - 1]; s[j - 1] = t; }
     for (int i = 0; i < nu; i++) lock_bucket(d.locks, s[i]);
   }
-  __device__ void ck_unlock_all(const u64* uq, int nu) {
-    if (d.phased) return;
+  __device__ void ck_unlock_all(const u64* uq, int nu, bool mut = true) {
+    if (d.phased && !mut) return;
     for (int i = 0; i < nu; i++) unlock_bucket(d.locks, uq[i]);
   }
 
@@ -867,13 +871,13 @@ struct Ctx {
     const int n = B();
     u64 uq[8];
     const int nu = ck_buckets(key, uq);
-    if (take_locks) ck_lock_all(uq, nu);
+    if (take_locks) ck_lock_all(uq, nu, false);
     i64 idx = -1;
     for (int i = 0; i < nu && idx < 0; i++) {
       Find r = scan_cells(uq[i] * (u64)n, n, key);
       if (r.idx >= 0) { idx = r.idx; val = r.val; }
     }
-    if (take_locks) ck_unlock_all(uq, nu);
+    if (take_locks) ck_unlock_all(uq, nu, false);
     return idx;
   }
 
