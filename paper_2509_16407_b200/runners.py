@@ -351,3 +351,44 @@ def run_ycsb(workload: str, universe: int = 1 << 24, ops: int = 1 << 26, capacit
     return {"workload": workload, "universe": universe, "ops": ops, "updates": int(is_up.sum()),
             "ms": ms, "mops": _mops(ops, ms), "missing_queries": missing, "final_values_exact": values_ok,
             "combine": combine}
+
+
+def run_phased_overhead(designs=("double", "double_md", "iceberg", "iceberg_md", "p2", "p2_md", "cuckoo",
+                                 "chaining"), capacity: int = 1 << 24, seed: int = 42, reps: int = 3) -> dict:
+    """Concurrent vs phased (BSP) query throughput per design (paper Table 1,
+    PAPER.md:1390-1415; reference runners.py:408-476): the same fill, then the
+    same 50/50 hit/miss query batch against a `mode="concurrent"` and a
+    `mode="phased"` table; overhead = 1 - concurrent / phased."""
+    from .tables import make_table
+    torch = _torch()
+    out = {}
+    for design in designs:
+        load = 0.85 if design.startswith("double") else (1.0 if design == "chaining" else 0.9)
+        res = {}
+        for mode in ("concurrent", "phased"):
+            cfg = TableConfig(design=design, capacity_slots=capacity if design != "chaining" else 7 * (capacity // 8),
+                              seed=seed, mode=mode)
+            t = make_table(cfg)
+            dev = t.device
+            n = int(t.capacity_slots * load)
+            keys = gen_uniform_keys(seed, n)
+            dk = _dev(keys, dev)
+            t.upsert_batch(dk, dk, check=False)
+            miss = gen_uniform_keys(derive_seed(seed, 0xFEED), n // 2)
+            q = np.concatenate([keys[: n // 2], miss])
+            np.random.default_rng(seed).shuffle(q)
+            dq = _dev(q, dev)
+            t.query_batch(dq, check=False)  # warm-up
+            best = 1e30
+            for _ in range(reps):
+                with _Timer() as tm:
+                    f, _v = t.query_batch(dq, check=False)
+                best = min(best, tm.ms)
+            hits = int(_np(f).astype(bool).sum())
+            res[mode] = {"query_mops": _mops(len(q), best), "hits": hits}
+            del t, dk, dq
+            torch.cuda.empty_cache()
+        c, p = res["concurrent"]["query_mops"], res["phased"]["query_mops"]
+        out[design] = {"concurrent_mops": c, "phased_mops": p, "overhead_pct": 100.0 * (1 - c / p) if p else 0.0,
+                       "same_hits": res["concurrent"]["hits"] == res["phased"]["hits"]}
+    return out

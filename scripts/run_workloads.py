@@ -52,6 +52,9 @@ for wl in ("A", "B", "C"):
     r = runners.run_ycsb(wl, universe=1 << (20 if quick else 24), ops=1 << (22 if quick else 26))
     out[f"ycsb_{wl}"] = r
     print("ycsb", r, flush=True)
+r = runners.run_phased_overhead(capacity=1 << (20 if quick else 24))
+out["table1_concurrent_vs_phased_query"] = r
+print("phased overhead", r, flush=True)
 from paper_2509_16407_b200.cache import run_cache_sweep
 r = run_cache_sweep(universe=1 << (18 if quick else 22), ratios=(0.1, 0.25, 0.5, 0.75, 0.9), queries_per_key=4.0,
                     batch=1 << 16)
