@@ -47,4 +47,44 @@ __device__ __forceinline__ void scan32_lines(const u64* cells, u64 lo, u64 key, 
   }
 }
 
+// Whole-bucket variant for mutations (reference _find_in_bucket plus
+// _used_and_free, openaddr.py:59-130): key match anywhere (a key never sits
+// past an EMPTY, so this equals the stopping scan), `used` = claimed cells of
+// the whole bucket, `hint` = first EMPTY/TOMB, `saw_empty` = any EMPTY.  The
+// second half is skipped once the key is found.
+template <bool RO>
+__device__ __forceinline__ void scan32_all(const u64* cells, u64 lo, u64 key, i64& idx, u64& val, int& used,
+                                           i64& hint, bool& saw_empty) {
+  idx = -1;
+  used = 0;
+  hint = -1;
+  saw_empty = false;
+#pragma unroll
+  for (int half = 0; half < 2; half++) {
+    u64 w[32];
+    const u64* p = cells + 2 * (lo + 16 * half);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      if (RO)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(w[4 * q]), "=l"(w[4 * q + 1]), "=l"(w[4 * q + 2]), "=l"(w[4 * q + 3])
+                     : "l"(p + 4 * q));
+      else
+        asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                     : "=l"(w[4 * q]), "=l"(w[4 * q + 1]), "=l"(w[4 * q + 2]), "=l"(w[4 * q + 3])
+                     : "l"(p + 4 * q) : "memory");
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j++) {
+      const u64 k = w[2 * j];
+      const i64 slot = (i64)(lo + 16 * half + j);
+      if (k == key) { idx = slot; val = w[2 * j + 1]; }
+      if (k == EMPTY || k == TOMB) { if (hint < 0) hint = slot; }
+      else used++;
+      saw_empty |= k == EMPTY;
+    }
+    if (idx >= 0) return;
+  }
+}
+
 }  // namespace ws
