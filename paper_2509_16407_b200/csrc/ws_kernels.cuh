@@ -44,7 +44,9 @@ __global__ void __launch_bounds__(kThreads) k_ops(Dev d, const u8* __restrict__ 
                                                   const u64* __restrict__ keys,
                                                   const u64* __restrict__ vals, u64 n, u8* status,
                                                   u64* vout, const u8* redo, u32* probes,
-                                                  u64* lock_acc, int conc_erase, int gated) {
+                                                  u64* lock_acc, int conc_erase, int gated,
+                                                  const u64* __restrict__ rlist = nullptr,
+                                                  const u64* __restrict__ rcount = nullptr) {
   if (gate_closed(d, gated)) return;
   Probe* pp = nullptr;
   Probe pr;
@@ -52,8 +54,12 @@ __global__ void __launch_bounds__(kThreads) k_ops(Dev d, const u8* __restrict__ 
   // conc_erase 2: the launch's erase count (k_count_erases) decides
   const bool conc = conc_erase == 2 ? ld_u32_relaxed(d.state + 4) != 0 : conc_erase != 0;
   Ctx<DES, BS, false, INSTR> c{d, pp, conc, ld_u32_relaxed(d.state)};
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-    if (redo && redo[i] != S_RETRY) continue;
+  // rlist: a compacted list of the batch indices to run (*rcount of them),
+  // so every lane of a warp has work (k_compact_retry)
+  const u64 nn = rcount ? *rcount : n;
+  for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < nn; t += (u64)gridDim.x * blockDim.x) {
+    const u64 i = rlist ? rlist[t] : t;
+    if (redo && !rlist && redo[i] != S_RETRY) continue;
     const u8 op = ops ? __ldg(ops + i) : uop;
     const u64 key = __ldg(keys + i);
     const u64 val = vals ? __ldg(vals + i) : 0ull;
@@ -103,6 +109,8 @@ struct OpsArgs {
   u64* lock_acc;
   int conc_erase, gated, instr, serial;
   cudaStream_t s;
+  const u64* rlist = nullptr;   // optional compacted index list (k_ops)
+  const u64* rcount = nullptr;
 };
 
 struct QueryArgs {
@@ -134,7 +142,7 @@ void launch_ops_t(const OpsArgs& a) {
   else
     k_ops<DES, BS, false><<<a.serial ? 1 : grid_for_table(a.n, a.d.nb), a.serial ? 1 : kThreads, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
                                                                 a.vout, a.redo, a.probes, a.lock_acc,
-                                                                a.conc_erase, a.gated);
+                                                                a.conc_erase, a.gated, a.rlist, a.rcount);
 }
 
 template <int DES, int BS>
