@@ -22,13 +22,13 @@ __global__ void __launch_bounds__(256) k_query_p2_lines(Dev d, const u64* __rest
     u64 val = 0;
     int used;
     bool saw_empty;
-    scan32_lines<RO>(d.cells, b0 * 32, key, idx, val, used, hint, saw_empty);
+    scan32_all<RO>(d.cells, b0 * 32, key, idx, val, used, hint, saw_empty);
     if (idx < 0) {
       bool te = te0 != 0;
       if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
       if (!(saw_empty && !te && used < d.shortcut)) {
         const u64 b1 = d.nbm(mix64(key ^ d.seeds[1]) >> 16);
-        if (b1 != b0) scan32_lines<RO>(d.cells, b1 * 32, key, idx, val, used, hint, saw_empty);
+        if (b1 != b0) scan32_all<RO>(d.cells, b1 * 32, key, idx, val, used, hint, saw_empty);
       }
     }
     if (found) found[i] = idx >= 0;
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) k_query_p2_lines(Dev d, const u64* __rest
 // P2 upsert (reference openaddr.py:370-418 with the serialisable routing of
 // Ctx::p2_upsert) in the warp-synchronous lock rounds of k_upsert_p2md_rounds
 // (ws_fast.cuh), with the bucket scans of a design without metadata: lock
-// b0, scan it a half-bucket at a time (scan32_lines); found -> merge; the
+// b0, scan it a half-bucket at a time (scan32_all); found -> merge; the
 // shortcut (never tombstoned, fewer than `shortcut` claimed cells before the
 // first EMPTY) claims b0's first free cell; otherwise lock and scan b1 and
 // claim in the less-used bucket (ties to b0), else FULL.  Exclusive plain
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) k_upsert_p2_rounds(Dev d, const u64* __re
           u64 old = 0;
           int used;
           bool se;
-          scan32_lines<false>(d.cells, b * 32, key, idx, old, used, hint, se);
+          scan32_all<false>(d.cells, b * 32, key, idx, old, used, hint, se);
           if (idx >= 0) {
             st_cell(d.cells + 2 * (u64)idx, key, apply_merge(merge, old, val));
             st = S_UPDATED;
