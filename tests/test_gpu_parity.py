@@ -161,7 +161,7 @@ def test_concurrent_fill_then_query_matches_oracle(design):
     np.testing.assert_array_equal(_np(got), oval)
 
 
-@pytest.mark.parametrize("design", ["p2_md", "p2", "double_md", "iceberg_md", "cuckoo", "chaining"])
+@pytest.mark.parametrize("design", ["p2_md", "p2", "double_md", "iceberg_md", "iceberg", "cuckoo", "chaining"])
 def test_concurrent_upsert_add_with_duplicate_keys(design):
     from paper_2509_16407_b200.workload import zipf_ranks
     cap = 1 << 15
@@ -552,5 +552,54 @@ def test_phased_mode_batches_match_oracle(design):
     st = _np(t.upsert_batch(_cuda(more), _cuda(more)))
     ost = o.upsert_batch(more, more)
     np.testing.assert_array_equal(st, ost)
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("design", ["p2", "p2_md", "iceberg", "iceberg_md", "double", "chaining"])
+def test_tombstoned_table_uniform_upserts_match_oracle(design):
+    """The per-design lock-round upsert kernels on a table that has
+    tombstones (fill 0.8, erase 30%, then one upsert-ADD launch of fresh keys
+    and surviving keys): the tombstones_ever path (no shortcut, reusable TOMB
+    cells, no whole-sector fill) must give the oracle's final map."""
+    cap = 1 << 16
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * 8192, seed=6)
+    t = _table(cfg)
+    o = _oracle(cfg)
+    n = int(t.capacity_slots * (0.8 if not design.startswith("double") else 0.75))
+    keys = _keys(21, n + n // 4)
+    base, fresh = keys[:n], keys[n:]
+    assert (_np(t.upsert_batch(_cuda(base), _cuda(base))) == 0).all()
+    o.upsert_batch(base, base)
+    gone = base[: int(n * 0.3)]
+    assert _np(t.erase_batch(_cuda(gone))).all()
+    o.erase_batch(gone)
+    live = base[int(n * 0.3):]
+    batch = np.concatenate([fresh, live[: len(live) // 2]])
+    np.random.default_rng(2).shuffle(batch)
+    vals = batch & np.uint64(0xFFF)
+    st = _np(t.upsert_batch(_cuda(batch), _cuda(vals), merge="add"))
+    ost = o.upsert_batch(batch, vals, merge="add")
+    np.testing.assert_array_equal(st, ost)
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
+
+
+def test_cuckoo_high_load_eviction_matches_oracle():
+    """Cuckoo to 0.95 in slices: most late inserts take eviction chains (the
+    compacted S_RETRY launch); same final contents as the oracle over the
+    keys that were not FULL, no duplicates."""
+    cap = 1 << 16
+    cfg = cfg_for("cuckoo", cap, seed=7)
+    t = _table(cfg)
+    keys = _keys(23, int(cap * 0.95))
+    full = np.zeros(len(keys), dtype=bool)
+    for part in np.array_split(np.arange(len(keys)), 8):
+        st = _np(t.upsert_batch(_cuda(keys[part]), _cuda(keys[part])))
+        assert not (st == 1).any() and int((st == 2).sum()) <= 8, np.bincount(st)
+        full[part] = st == 2
+    o = _oracle(cfg)
+    kin = keys[~full]
+    o.upsert_batch(kin, kin)
     assert dict(t.items()) == o.as_dict()
     assert t.duplicate_scan() == {}
