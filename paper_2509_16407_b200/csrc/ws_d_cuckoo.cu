@@ -6,10 +6,46 @@
 
 namespace ws {
 
-// 32 bytes (two cells) in one LDG.E.ENL2.256
-__device__ __forceinline__ void ld_cells2(const u64* p, u64& k0, u64& v0, u64& k1, u64& v1) {
+__device__ __forceinline__ void ld32b(const u64* p, u64* w) {
   asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
-               : "=l"(k0), "=l"(v0), "=l"(k1), "=l"(v1) : "l"(p) : "memory");
+               : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(p) : "memory");
+}
+// Scan of one 8-cell bucket (a 128-byte line) in hash-slot order, stopping
+// at the key or the first EMPTY, in stages of 32-byte sectors: the first
+// sector alone (one request; at low load it usually holds an EMPTY), then
+// (STAGED) the second alone, then the remaining sectors together -- fewer
+// round trips than sector by sector, at most one extra request.  The query
+// (loads around 0.9, most buckets need every sector) takes the rest in one
+// stage; the upsert, whose fills start from an empty table, takes two.
+// `fr` = first reusable cell (TOMB / EMPTY).
+template <bool STAGED>
+__device__ __forceinline__ void scan_line8(const u64* p, u64 lo, u64 key, i64& hit, u64& val, i64& fr) {
+  u64 w[16];
+  bool stop = false;
+  auto scan = [&](int j0, int j1) {
+#pragma unroll
+    for (int j = j0; j < j1; j++) {
+      if (!stop) {
+        if (w[2 * j] == key) { hit = (i64)(lo + j); val = w[2 * j + 1]; stop = true; }
+        else if (w[2 * j] == EMPTY) { if (fr < 0) fr = (i64)(lo + j); stop = true; }
+        else if (w[2 * j] == TOMB) { if (fr < 0) fr = (i64)(lo + j); }
+      }
+    }
+  };
+  ld32b(p, w);
+  scan(0, 2);
+  if (stop) return;
+  if (STAGED) {
+    ld32b(p + 4, w + 4);
+    scan(2, 4);
+    if (stop) return;
+  } else {
+    ld32b(p + 4, w + 4);
+  }
+  ld32b(p + 8, w + 8);
+  ld32b(p + 12, w + 12);
+  if (!STAGED) scan(2, 4);
+  scan(4, 8);
 }
 
 // Cuckoo query (reference cuckoo.py:185-198): take the locks of the key's
@@ -54,18 +90,9 @@ __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* _
       const bool ready = pending && (!locked || held == nu);
       if (ready) {
         for (int q = 0; q < nu && !hit; q++) {
-          const u64* base = d.cells + 2 * (uq[q] * 8);
-          bool empty = false;
-#pragma unroll
-          for (int h = 0; h < 4; h++) {
-            if (empty || hit) break;
-            u64 k0, v0, k1, v1;
-            ld_cells2(base + 4 * h, k0, v0, k1, v1);
-            if (k0 == key) { hit = true; val = v0; }
-            else if (k0 == EMPTY) empty = true;
-            else if (k1 == key) { hit = true; val = v1; }
-            else if (k1 == EMPTY) empty = true;
-          }
+          i64 h = -1, fr = -1;
+          scan_line8<false>(d.cells + 2 * (uq[q] * 8), uq[q] * 8, key, h, val, fr);
+          hit = h >= 0;
         }
         pending = false;
       }
@@ -135,21 +162,7 @@ __global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* 
         for (int q = 0; q < nu && hit < 0; q++) {
           const u64 lo = uq[q] * 8;
           i64 fr = -1;
-          bool empty = false;
-#pragma unroll
-          for (int h = 0; h < 4; h++) {
-            if (empty || hit >= 0) break;
-            u64 k[2], v[2];
-            ld_cells2(d.cells + 2 * (lo + 2 * h), k[0], v[0], k[1], v[1]);
-#pragma unroll
-            for (int e = 0; e < 2; e++) {
-              if (empty || hit >= 0) break;
-              const u64 slot = lo + 2 * h + e;
-              if (k[e] == key) { hit = (i64)slot; old = v[e]; }
-              else if (k[e] == EMPTY) { if (fr < 0) fr = (i64)slot; empty = true; }
-              else if (k[e] == TOMB) { if (fr < 0) fr = (i64)slot; }
-            }
-          }
+          scan_line8<true>(d.cells + 2 * lo, lo, key, hit, old, fr);
           if (free_at < 0 && fr >= 0) free_at = fr;
         }
         if (hit >= 0) {
