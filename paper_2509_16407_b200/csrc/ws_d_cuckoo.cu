@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* 
 
 // Warp-aggregated compaction of the S_RETRY ops into an index list (order
 // within a warp kept, across warps arbitrary: the ops are concurrent anyway).
-__global__ void __launch_bounds__(256) k_compact_retry(const u8* __restrict__ st, u64 n, u64* list, u64* count) {
+__global__ void __launch_bounds__(256) k_compact_retry(const u8* __restrict__ st, u64 n, u32* list, u32* count) {
   const int lane = threadIdx.x & 31;
   for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n;
        base += (u64)gridDim.x * blockDim.x) {
@@ -201,10 +201,10 @@ __global__ void __launch_bounds__(256) k_compact_retry(const u8* __restrict__ st
     const bool r = i < n && st[i] == S_RETRY;
     const u32 m = __ballot_sync(0xFFFFFFFFu, r);
     if (!m) continue;
-    u64 at = 0;
-    if (lane == 0) at = atomicAdd((unsigned long long*)count, (unsigned long long)__popc(m));
+    u32 at = 0;
+    if (lane == 0) at = atomicAdd(count, (u32)__popc(m));
     at = __shfl_sync(0xFFFFFFFFu, at, 0);
-    if (r) list[at + __popc(m & ((1u << lane) - 1))] = i;
+    if (r) list[at + __popc(m & ((1u << lane) - 1))] = (u32)i;
   }
 }
 
@@ -223,9 +223,9 @@ static void cuckoo_ops(const OpsArgs& a, bool def) {
       lo.redo = st;  // the generic kernel runs only the S_RETRY ops (eviction chains)
       // compacted, so the eviction searches fill whole warps instead of the
       // ~1/3 of lanes whose buckets were full
-      u64* rl = nullptr;
-      if (cudaMallocAsync((void**)&rl, 8 * (a.n + 1), a.s) == cudaSuccess) {
-        cudaMemsetAsync(rl + a.n, 0, 8, a.s);
+      u32* rl = nullptr;
+      if (a.n < 0xFFFFFFFFull && cudaMallocAsync((void**)&rl, 4 * (a.n + 1), a.s) == cudaSuccess) {
+        cudaMemsetAsync(rl + a.n, 0, 4, a.s);
         k_compact_retry<<<(unsigned)std::max<u64>(std::min<u64>((a.n + 255) / 256, (u64)kSMs * 8), 1), 256, 0,
                           a.s>>>(st, a.n, rl, rl + a.n);
         lo.rlist = rl;

@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(kThreads) k_ops(Dev d, const u8* __restrict__ 
                                                   const u64* __restrict__ vals, u64 n, u8* status,
                                                   u64* vout, const u8* redo, u32* probes,
                                                   u64* lock_acc, int conc_erase, int gated,
-                                                  const u64* __restrict__ rlist = nullptr,
-                                                  const u64* __restrict__ rcount = nullptr) {
+                                                  const u32* __restrict__ rlist = nullptr,
+                                                  const u32* __restrict__ rcount = nullptr) {
   if (gate_closed(d, gated)) return;
   Probe* pp = nullptr;
   Probe pr;
@@ -109,8 +109,8 @@ struct OpsArgs {
   u64* lock_acc;
   int conc_erase, gated, instr, serial;
   cudaStream_t s;
-  const u64* rlist = nullptr;   // optional compacted index list (k_ops)
-  const u64* rcount = nullptr;
+  const u32* rlist = nullptr;   // optional compacted index list (k_ops; batches < 2^32)
+  const u32* rcount = nullptr;
 };
 
 struct QueryArgs {
