@@ -382,8 +382,8 @@ def run_ours(args, rank, world):
                 "insert_requests_per_op": INSERT_REQ, "query_requests_per_op": QUERY_REQ,
                 "insert_achieved": round(n * INSERT_REQ / ms_ins / 1e6, 2),
                 "query_achieved": round(n * QUERY_REQ / ms_qry / 1e6, 2),
-                "insert_frac": round(n * INSERT_REQ / ms_ins / 1e6 / ceiling, 4),
-                "query_frac": round(n * QUERY_REQ / ms_qry / 1e6 / ceiling, 4),
+                "insert_frac": round(n * INSERT_REQ / ms_ins / 1e6 / ceiling, 4) if ceiling else None,
+                "query_frac": round(n * QUERY_REQ / ms_qry / 1e6 / ceiling, 4) if ceiling else None,
             },
             # SURVEY 8(d) also asks for the fraction of the 8 TB/s nominal HBM3e figure
             "nominal_peak_gbs": 8000.0,
