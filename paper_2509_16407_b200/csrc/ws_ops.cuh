@@ -399,13 +399,21 @@ struct Ctx {
   __device__ u64 dbl_next(u64 b, u64 sm) const { const u64 x = b + sm; return x >= d.nb ? x - d.nb : x; }
 
   __device__ u8 dbl_upsert(u64 key, u64 val, int merge) {
+    const u64 b0 = hb(0, key, d.nbm);
+    lock(b0);
+    const u8 st = dbl_upsert_held(key, val, merge);
+    unlock(b0);
+    return st;
+  }
+  // the body of dbl_upsert with the primary-bucket lock already held (also
+  // run by the lock-round kernel of ws_d_double_md.cu)
+  __device__ u8 dbl_upsert_held(u64 key, u64 val, int merge) {
     const u64 h0 = mix64(key ^ d.seeds[0]);
     const u64 b0 = d.nbm(h0 >> 16);
     const u16 tag = md_tag(h0);
     const u64 sm = (mix64(key ^ d.seeds[1]) | 1ull) % d.nb;  // (b+step)%nb without 2^64 wrap
     const u64 len = dbl_len();
     u8 st;
-    lock(b0);
     for (;;) {
       i64 fb = -1, fh = -1;
       u64 b = b0;
@@ -421,7 +429,6 @@ struct Ctx {
       if (fb < 0) { st = S_FULL; break; }
       if (claim_publish((u64)fb, fh, key, val, tag) >= 0) { st = S_INSERTED; break; }
     }
-    unlock(b0);
     return st;
   }
 

@@ -556,7 +556,7 @@ def test_phased_mode_batches_match_oracle(design):
     assert t.duplicate_scan() == {}
 
 
-@pytest.mark.parametrize("design", ["p2", "p2_md", "iceberg", "iceberg_md", "double", "chaining"])
+@pytest.mark.parametrize("design", ["p2", "p2_md", "iceberg", "iceberg_md", "double", "double_md", "chaining"])
 def test_tombstoned_table_uniform_upserts_match_oracle(design):
     """The per-design lock-round upsert kernels on a table that has
     tombstones (fill 0.8, erase 30%, then one upsert-ADD launch of fresh keys
