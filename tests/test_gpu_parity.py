@@ -603,3 +603,46 @@ def test_cuckoo_high_load_eviction_matches_oracle():
     o.upsert_batch(kin, kin)
     assert dict(t.items()) == o.as_dict()
     assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "chaining"])
+@pytest.mark.parametrize("with_replace", [False, True])
+def test_combined_mixed_batch_matches_sequential_oracle(design, with_replace):
+    """Mixed batch with combining (the aging / YCSB path): Zipf-hot upsert-ADD
+    (duplicates), optionally REPLACE upserts with duplicates (op bytes 0x00
+    and 0x20 around the erase / query bytes), erases and present / absent
+    queries, roles key-disjoint.  Combining is one serial order of the batch
+    and, for these roles, the index order: statuses, values and the final map
+    equal the oracle's sequential replay exactly."""
+    from paper_2509_16407_b200.tables import OP_ERASE, OP_QUERY, OP_UPSERT
+    from paper_2509_16407_b200.workload import zipf_ranks
+    cap = 1 << 15
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * 4096, seed=12)
+    t = _table(cfg)
+    o = _oracle(cfg)
+    fill = int(t.capacity_slots * 0.6)
+    base = _keys(31, fill)
+    t.upsert_batch(_cuda(base), _cuda(base & np.uint64(0xFFFF)))
+    o.upsert_batch(base, base & np.uint64(0xFFFF))
+    hot = np.concatenate([base[:500], _keys(32, 500)])  # half present, half new
+    add_keys = hot[zipf_ranks(len(hot), 6000, 0.99, seed=5) - 1]
+    parts_ops = [np.full(len(add_keys), OP_UPSERT | (2 << 4))]
+    parts_keys = [add_keys]
+    if with_replace:
+        rep = _keys(33, 300)
+        rep_keys = rep[np.random.default_rng(4).integers(0, 300, 2000)]
+        parts_ops.append(np.full(len(rep_keys), OP_UPSERT))
+        parts_keys.append(rep_keys)
+    parts_ops += [np.full(800, OP_ERASE), np.full(800, OP_QUERY), np.full(800, OP_QUERY)]
+    parts_keys += [base[1000:1800], base[2000:2800], _keys(34, 800)]
+    ops = np.concatenate(parts_ops).astype(np.uint8)
+    keys = np.concatenate(parts_keys)
+    vals = (np.arange(len(keys), dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(44)
+    perm = np.random.default_rng(6).permutation(len(keys))
+    ops, keys, vals = ops[perm], keys[perm], vals[perm]
+    st, vo = t.mixed_batch(_cuda(ops), _cuda(keys), _cuda(vals), combine=True)
+    ost, ovo = o.mixed_batch(ops, keys, vals)
+    bad = np.nonzero((_np(st) != ost) | (_np(vo) != ovo))[0]
+    assert bad.size == 0, [(int(ops[i]), int(_np(st)[i]), int(ost[i])) for i in bad[:10]]
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
