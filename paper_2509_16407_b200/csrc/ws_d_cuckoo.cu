@@ -48,6 +48,66 @@ __device__ __forceinline__ void scan_line8(const u64* p, u64 lo, u64 key, i64& h
   scan(4, 8);
 }
 
+// Per-op bucket set of the lock-round query with compile-time capacity W
+// (3 for the default table, 8 otherwise): hash-order distinct buckets in uq
+// (dict.fromkeys), ascending copy in srt (unused entries sort last as ~0).
+// Every loop runs to W with predicates, so the arrays stay in registers
+// (the upsert keeps its runtime-bounded arrays: measured no faster there).
+template <int W>
+__device__ __forceinline__ int ck_setup(const Dev& d, bool pending, u64 key, u64 (&uq)[W], u64 (&srt)[W]) {
+  const int ways = W == 3 ? 3 : d.ways;
+  int nu = 0;
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    uq[w] = ~0ull;
+    if (pending && w < ways) {
+      const u64 b = d.nbm(mix64(key ^ d.seeds[w]) >> 16);
+      bool dup = false;
+#pragma unroll
+      for (int j = 0; j < W; j++) dup |= j < nu && uq[j] == b;
+      if (!dup) {
+#pragma unroll
+        for (int j = 0; j < W; j++)
+          if (j == nu) uq[j] = b;
+        nu++;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < W; j++) srt[j] = j < nu ? uq[j] : ~0ull;
+#pragma unroll
+  for (int a = 0; a < W; a++)
+#pragma unroll
+    for (int b = 0; b + 1 < W - a; b++)
+      if (srt[b] > srt[b + 1]) { const u64 t = srt[b]; srt[b] = srt[b + 1]; srt[b + 1] = t; }
+  return nu;
+}
+// uq[q] without dynamic indexing (a select chain keeps the array in registers)
+template <int W>
+__device__ __forceinline__ u64 ck_pick(const u64 (&a)[W], int q) {
+  u64 r = a[0];
+#pragma unroll
+  for (int j = 1; j < W; j++)
+    if (q == j) r = a[j];
+  return r;
+}
+// try-lock the sorted buckets from `held` on, stopping at the first failure
+template <int W>
+__device__ __forceinline__ int ck_trylock_prefix(const Dev& d, const u64 (&srt)[W], int nu, int held) {
+#pragma unroll
+  for (int j = 0; j < W; j++)
+    if (j == held && j < nu && try_lock_bucket(d.locks, srt[j])) held++;
+  return held;
+}
+template <int W>
+__device__ __forceinline__ void ck_release(const Dev& d, const u64 (&srt)[W], int nu) {
+#pragma unroll
+  for (int q = 0; q < W; q++)
+    if (q < nu)
+      asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(d.locks + (srt[q] >> 5)),
+                   "r"(~(1u << (srt[q] & 31))) : "memory");
+}
+
 // Cuckoo query (reference cuckoo.py:185-198): take the locks of the key's
 // distinct buckets in ascending order, scan them in hash order (stopping at
 // the first EMPTY, sync.py:184-207), release.  One thread per op in
@@ -57,6 +117,7 @@ __device__ __forceinline__ void scan_line8(const u64* p, u64 lo, u64 key, i64& h
 // lanes of a warp racing for the same lowest lock get exactly one winner);
 // lanes holding all their locks scan with 32-byte loads, then the warp issues
 // one fence and the finished lanes release with relaxed reductions.
+template <int W>
 __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* __restrict__ keys, u64 n,
                                                              u64* vout, u8* found, int gated) {
   if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
@@ -67,31 +128,21 @@ __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* _
     const u64 i = c * 32 + lane;
     bool pending = i < n;
     const u64 key = pending ? __ldg(keys + i) : 0;
-    u64 uq[8], srt[8];
-    int nu = 0;
-    if (pending) {
-      for (int w = 0; w < d.ways; w++) {  // dict.fromkeys(buckets): hash order, deduplicated
-        const u64 b = d.nbm(mix64(key ^ d.seeds[w]) >> 16);
-        bool dup = false;
-        for (int j = 0; j < nu; j++) dup |= uq[j] == b;
-        if (!dup) uq[nu++] = b;
-      }
-      for (int j = 0; j < nu; j++) srt[j] = uq[j];
-      for (int a = 1; a < nu; a++)
-        for (int b = a; b > 0 && srt[b - 1] > srt[b]; b--) { const u64 t = srt[b]; srt[b] = srt[b - 1]; srt[b - 1] = t; }
-    }
+    u64 uq[W], srt[W];
+    const int nu = ck_setup<W>(d, pending, key, uq, srt);
     int held = 0;
     bool hit = false;
     u64 val = 0;
     unsigned backoff = 64;
     while (__any_sync(0xFFFFFFFFu, pending)) {
-      if (pending && locked)
-        while (held < nu && try_lock_bucket(d.locks, srt[held])) held++;
+      if (pending && locked) held = ck_trylock_prefix<W>(d, srt, nu, held);
       const bool ready = pending && (!locked || held == nu);
       if (ready) {
+#pragma unroll 1
         for (int q = 0; q < nu && !hit; q++) {
+          const u64 b = ck_pick<W>(uq, q);
           i64 h = -1, fr = -1;
-          scan_line8<false>(d.cells + 2 * (uq[q] * 8), uq[q] * 8, key, h, val, fr);
+          scan_line8<false>(d.cells + 2 * (b * 8), b * 8, key, h, val, fr);
           hit = h >= 0;
         }
         pending = false;
@@ -99,11 +150,7 @@ __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* _
       if (locked) {
         __syncwarp();
         fence_acq_rel();
-        if (ready) {
-          for (int q = 0; q < nu; q++)
-            asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(d.locks + (srt[q] >> 5)),
-                         "r"(~(1u << (srt[q] & 31))) : "memory");
-        }
+        if (ready) ck_release<W>(d, srt, nu);
       }
       if (pending) {
         __nanosleep(backoff + 8 * lane);
@@ -243,7 +290,10 @@ static void cuckoo_query(const QueryArgs& a, bool def) {
   if (def && a.d.ways <= 8 && a.d.tune_qilp > 0) {
     u64 g = (a.n + 255) / 256;
     g = std::max<u64>(std::min<u64>(g, (u64)kSMs * 8), 1);
-    k_query_cuckoo_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);
+    if (a.d.ways == 3)
+      k_query_cuckoo_rounds<3><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);
+    else
+      k_query_cuckoo_rounds<8><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);
     return;
   }
   if (def) launch_query_t<D_CUCKOO, 8>(a); else launch_query_t<D_CUCKOO, 0>(a);
@@ -254,7 +304,8 @@ static void cuckoo_locate(const LocateArgs& a, bool def) {
 static void cuckoo_preload(bool def) {
   if (!def) { preload_t<D_CUCKOO, 0>(); return; }
   preload_t<D_CUCKOO, 8>();
-  preload_fn(k_query_cuckoo_rounds);
+  preload_fn(k_query_cuckoo_rounds<3>);
+  preload_fn(k_query_cuckoo_rounds<8>);
   preload_fn(k_upsert_cuckoo_rounds);
   preload_fn(k_compact_retry);
 }
