@@ -846,6 +846,7 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.tune_l2pol = 2;
   d.tune_upsert = 4;
   d.tune_occ = 0;
+  d.ck_resume = 0;
   t->tune_bulk = 0;  // measured slower than the per-op kernel at 2^28
   t->tune_bulk_gb = -1;
   t->maybe_tomb = false;

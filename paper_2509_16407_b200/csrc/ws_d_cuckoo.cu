@@ -268,6 +268,7 @@ static void cuckoo_ops(const OpsArgs& a, bool def) {
       OpsArgs lo = a;
       lo.status = st;
       lo.redo = st;  // the generic kernel runs only the S_RETRY ops (eviction chains)
+      lo.d.ck_resume = 1;  // ...starting at their eviction search
       // compacted, so the eviction searches fill whole warps instead of the
       // ~1/3 of lanes whose buckets were full
       u32* rl = nullptr;

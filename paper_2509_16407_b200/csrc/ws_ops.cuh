@@ -45,6 +45,10 @@ struct Dev {
   int tune_l2pol;  // 1: tag loads evict_last, cell loads evict_first
   int tune_upsert; // P2-MD upsert kernel: 0 generic one-thread-per-op, 1 lane pair, 2/3 rounds
   int tune_occ;    // minimum resident CTAs per SM requested from ptxas (register cap)
+  // cuckoo: this launch continues ops whose first attempt (the locked scan
+  // that found every bucket full) already ran in k_upsert_cuckoo_rounds, so
+  // ck_upsert starts at the eviction search (launch-local, never stored)
+  int ck_resume;
   // delay injection at the reference's scheduling-hook stages
   // (tables/base.py:66-69, bench/adversarial.py:40-93): with probability
   // delay_p16/65536 a stage sleeps up to delay_ns; 0 = off (generic kernels)
@@ -837,23 +841,25 @@ struct Ctx {
     u64 uq[8];
     const int nu = ck_buckets(key, uq);
     for (int attempt = 0; attempt < CUCKOO_RETRIES; attempt++) {
-      ck_lock_all(uq, nu);
-      i64 free_at = -1;
-      u8 st = 0xFF;
-      for (int i = 0; i < nu && st == 0xFF; i++) {
-        Find r = scan_cells(uq[i] * (u64)n, n, key);
-        if (r.idx >= 0) st = update(r.idx, key, r.val, val, merge);
-        else if (free_at < 0 && r.hint >= 0) free_at = r.hint;
-      }
-      if (st == 0xFF && free_at >= 0) {
-        if (publish_cell(cell((u64)free_at), key, val)) {
-          touch(16 * (u64)free_at);
-          st = S_INSERTED;
+      if (attempt > 0 || !d.ck_resume) {
+        ck_lock_all(uq, nu);
+        i64 free_at = -1;
+        u8 st = 0xFF;
+        for (int i = 0; i < nu && st == 0xFF; i++) {
+          Find r = scan_cells(uq[i] * (u64)n, n, key);
+          if (r.idx >= 0) st = update(r.idx, key, r.val, val, merge);
+          else if (free_at < 0 && r.hint >= 0) free_at = r.hint;
         }
+        if (st == 0xFF && free_at >= 0) {
+          if (publish_cell(cell((u64)free_at), key, val)) {
+            touch(16 * (u64)free_at);
+            st = S_INSERTED;
+          }
+        }
+        ck_unlock_all(uq, nu);
+        if (st != 0xFF) return st;
+        if (free_at >= 0) continue;  // lost a race for the free cell: retry
       }
-      ck_unlock_all(uq, nu);
-      if (st != 0xFF) return st;
-      if (free_at >= 0) continue;  // lost a race for the free cell: retry
       if (d.depth >= 1) {
         u64 mv1[4];
         const int r1 = ck_find_path1(uq, nu, mv1);
