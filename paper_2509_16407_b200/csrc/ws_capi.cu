@@ -445,6 +445,12 @@ __global__ void k_comb_gather(const u64* keys, const u32* order, u64 n, u64* out
     out[j] = keys[order[j]];
 }
 
+// 32-bit sort key for commutative combining: the high half of mix64(key)
+__global__ void k_comb_hash32(const u64* keys, u64 n, u32* h) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    h[i] = (u32)(mix64(keys[i]) >> 32);
+}
+
 __global__ void k_comb_heads(const u64* sk, const u32* si, const u8* ops, u8 uop, const u64* vals, u64 n,
                              u32* head, OpVal* ov) {
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
@@ -532,7 +538,29 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
     WS_CK(cudaMemcpyAsync(idx, si, 4 * n, cudaMemcpyDeviceToDevice, s));
     sort_keys = keys_by_op;
   }
-  cub::DeviceRadixSort::SortPairs(tmp, tb, sort_keys, sk, idx, si, (int64_t)n, 0, 64, s);
+  // Uniform ADD / MAX / MIN batches sort on 32 hash bits (4 onesweep passes
+  // instead of 8).  Keys sharing the hash may interleave, so one key can form
+  // several runs; each run is folded and applied on its own, which for a
+  // commutative merge is still one serial order of the batch (one INSERTED
+  // per new key, the same final value).  REPLACE / KEEP (order-sensitive)
+  // and mixed batches keep the full 64-bit key sort.
+  const int um = uop >> 4;
+  const bool hash_sort = !ops && (um == M_ADD || um == M_MAX || um == M_MIN);
+  if (hash_sort) {
+    u32 *h = nullptr, *hs = nullptr;
+    size_t tbh = 0;
+    WS_CK(cudaMallocAsync((void**)&h, 4 * n, s));
+    WS_CK(cudaMallocAsync((void**)&hs, 4 * n, s));
+    cub::DeviceRadixSort::SortPairs(nullptr, tbh, h, hs, idx, si, (int64_t)n, 0, 32, s);
+    void* tmph = nullptr;
+    WS_CK(cudaMallocAsync(&tmph, tbh + 16, s));
+    k_comb_hash32<<<grid_for(n), kThreads, 0, s>>>(keys, n, h);
+    cub::DeviceRadixSort::SortPairs(tmph, tbh, h, hs, idx, si, (int64_t)n, 0, 32, s);
+    k_comb_gather<<<grid_for(n), kThreads, 0, s>>>(keys, si, n, sk);
+    for (void* p : {(void*)h, (void*)hs, tmph}) cudaFreeAsync(p, s);
+  } else {
+    cub::DeviceRadixSort::SortPairs(tmp, tb, sort_keys, sk, idx, si, (int64_t)n, 0, 64, s);
+  }
   k_comb_heads<<<grid_for(n), kThreads, 0, s>>>(sk, si, ops, uop, vals, n, head, ov);
   cub::DeviceScan::InclusiveSum(tmp, tb2, head, seg, (int64_t)n, s);
   cub::DeviceReduce::ReduceByKey(tmp, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
