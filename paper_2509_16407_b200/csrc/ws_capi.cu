@@ -453,6 +453,8 @@ __global__ void k_upsert_range(const u8* op_sorted, u64 n, u32* lohi) {
     const bool last = up && (j + 1 == n || (op_sorted[j + 1] & 15) != OP_UPSERT);
     if (first) atomicMin(lohi, (u32)j);
     if (last) atomicMax(lohi + 1, (u32)(j + 1));
+    const int m = op_sorted[j] >> 4;
+    if (first && m != M_ADD && m != M_MAX && m != M_MIN) atomicOr(lohi + 2, 1u);  // order-sensitive merge
   }
 }
 
@@ -519,7 +521,7 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   WS_CK(cudaMallocAsync((void**)&si, 4 * n, s));
   WS_CK(cudaMallocAsync((void**)&head, 4 * n, s));
   WS_CK(cudaMallocAsync((void**)&seg, 4 * n, s));
-  WS_CK(cudaMallocAsync((void**)&uniq, 4 * n, s));
+  WS_CK(cudaMallocAsync((void**)&uniq, 4 * std::max<u64>(n, 4), s));
   WS_CK(cudaMallocAsync((void**)&ov, sizeof(OpVal) * n, s));
   WS_CK(cudaMallocAsync((void**)&agg, sizeof(OpVal) * n, s));
   WS_CK(cudaMallocAsync((void**)&nruns, 8, s));
@@ -543,6 +545,7 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   const size_t tmax = std::max(std::max(tb0, tb), std::max(tb2, tb3)) + 16;
   WS_CK(cudaMallocAsync(&tmp, tmax, s));
   u64 lo = 0, hi = n;
+  bool span_commutative = false;
   if (ops) {
     // idx -> si ordered by op (stable); gather keys in that order; si -> idx
     cub::DeviceRadixSort::SortPairs(tmp, tb0, ops, op_sorted, idx, si, (int64_t)n, 0, 8, s);
@@ -552,15 +555,16 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
     // only the upserts need key order (every other op is its own group): the
     // 64-bit key sort covers just the span of upsert op bytes (one host read
     // of the span; YCSB-A batch 4.2 -> 3.5 ms)
-    u32* lohi = (u32*)nruns;
+    u32* lohi = (u32*)uniq;  // scratch until the reduce-by-key below
     WS_CK(cudaMemsetAsync(lohi, 0xFF, 4, s));
-    WS_CK(cudaMemsetAsync(lohi + 1, 0, 4, s));
+    WS_CK(cudaMemsetAsync(lohi + 1, 0, 8, s));
     k_upsert_range<<<grid_for(n), kThreads, 0, s>>>(op_sorted, n, lohi);
-    WS_CK(cudaMemcpyAsync(t->h_pin, lohi, 8, cudaMemcpyDeviceToHost, s));
+    WS_CK(cudaMemcpyAsync(t->h_pin, lohi, 12, cudaMemcpyDeviceToHost, s));
     WS_CK(cudaStreamSynchronize(s));
     const u32* hl = (const u32*)t->h_pin;
     lo = hl[0] == 0xFFFFFFFFu ? 0 : hl[0];
     hi = hl[0] == 0xFFFFFFFFu ? 0 : hl[1];
+    span_commutative = hl[2] == 0;
     if (lo > 0) {
       WS_CK(cudaMemcpyAsync(sk, keys_by_op, 8 * lo, cudaMemcpyDeviceToDevice, s));
       WS_CK(cudaMemcpyAsync(si, idx, 4 * lo, cudaMemcpyDeviceToDevice, s));
@@ -577,18 +581,19 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   // per new key, the same final value).  REPLACE / KEEP (order-sensitive)
   // and mixed batches keep the full 64-bit key sort.
   const int um = uop >> 4;
-  const bool hash_sort = !ops && (um == M_ADD || um == M_MAX || um == M_MIN);
-  if (hash_sort) {
+  const bool hash_sort = ops ? span_commutative : (um == M_ADD || um == M_MAX || um == M_MIN);
+  if (hash_sort && hi > lo) {
+    const u64 m = hi - lo;
     u32 *h = nullptr, *hs = nullptr;
     size_t tbh = 0;
-    WS_CK(cudaMallocAsync((void**)&h, 4 * n, s));
-    WS_CK(cudaMallocAsync((void**)&hs, 4 * n, s));
-    cub::DeviceRadixSort::SortPairs(nullptr, tbh, h, hs, idx, si, (int64_t)n, 0, 32, s);
+    WS_CK(cudaMallocAsync((void**)&h, 4 * m, s));
+    WS_CK(cudaMallocAsync((void**)&hs, 4 * m, s));
+    cub::DeviceRadixSort::SortPairs(nullptr, tbh, h, hs, idx + lo, si + lo, (int64_t)m, 0, 32, s);
     void* tmph = nullptr;
     WS_CK(cudaMallocAsync(&tmph, tbh + 16, s));
-    k_comb_hash32<<<grid_for(n), kThreads, 0, s>>>(keys, n, h);
-    cub::DeviceRadixSort::SortPairs(tmph, tbh, h, hs, idx, si, (int64_t)n, 0, 32, s);
-    k_comb_gather<<<grid_for(n), kThreads, 0, s>>>(keys, si, n, sk);
+    k_comb_hash32<<<grid_for(m), kThreads, 0, s>>>(sort_keys + lo, m, h);
+    cub::DeviceRadixSort::SortPairs(tmph, tbh, h, hs, idx + lo, si + lo, (int64_t)m, 0, 32, s);
+    k_comb_gather<<<grid_for(m), kThreads, 0, s>>>(keys, si + lo, m, sk + lo);
     for (void* p : {(void*)h, (void*)hs, tmph}) cudaFreeAsync(p, s);
   } else if (hi > lo) {
     cub::DeviceRadixSort::SortPairs(tmp, tb, sort_keys + lo, sk + lo, idx + lo, si + lo, (int64_t)(hi - lo), 0, 64,
