@@ -565,6 +565,15 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
     lo = hl[0] == 0xFFFFFFFFu ? 0 : hl[0];
     hi = hl[0] == 0xFFFFFFFFu ? 0 : hl[1];
     span_commutative = hl[2] == 0;
+    if (hi <= lo) {
+      // no upserts at all (e.g. YCSB-C): nothing to fold -- run the batch as is
+      for (void* p : {(void*)sk, (void*)idx, (void*)si, (void*)head, (void*)seg, (void*)uniq, (void*)ov,
+                      (void*)agg, (void*)nruns, tmp, (void*)op_sorted, (void*)keys_by_op})
+        if (p) cudaFreeAsync(p, s);
+      return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s,
+                              (flags & ~(WS_F_COMBINE | WS_F_SYNC_CHECK)) | WS_F_NO_CHECK, has_erase, has_upsert,
+                              false);
+    }
     if (lo > 0) {
       WS_CK(cudaMemcpyAsync(sk, keys_by_op, 8 * lo, cudaMemcpyDeviceToDevice, s));
       WS_CK(cudaMemcpyAsync(si, idx, 4 * lo, cudaMemcpyDeviceToDevice, s));
