@@ -24,6 +24,9 @@
  *   ws_duplicate_scan         HashTable.duplicate_scan()       tables/base.py:151-156
  *   ws_checksum               (new) size-independent content digest for parity at 2^28+
  *   ws_export_raw             slots.key_at / tags.get / arena words (test introspection)
+ *   ws_read_range             slots.snapshot / find_free / used_count / tags.get over a
+ *                             bucket range (sync.py:279-288, 184-207, 426-473) without a
+ *                             whole-table copy
  *   ws_info                   storage_report / arena.next_node / _tombstones_ever
  *   ws_tune                   (new) performance knobs, no semantic effect
  *   ws_partition/ws_unpermute (new) owner routing of the hash-sharded multi-GPU table
@@ -148,6 +151,11 @@ WS_API int ws_duplicate_scan(ws_table *t, uint64_t *dup_keys, uint64_t *dup_coun
 WS_API int ws_checksum(ws_table *t, uint64_t out[4], void *stream);
 WS_API int ws_export_raw(ws_table *t, uint64_t *words, uint64_t nwords, uint16_t *tags,
                   void *stream);
+/* words [first_word, first_word + nwords) of the cell array (2 per slot, or the
+ * chaining node arena) and tags [first_tag, first_tag + ntags) into host or
+ * device buffers; WS_ERR_ARG when a range runs past the table */
+WS_API int ws_read_range(ws_table *t, uint64_t first_word, uint64_t nwords, uint64_t *words,
+                  uint64_t first_tag, uint64_t ntags, uint16_t *tags, void *stream);
 WS_API int ws_info(ws_table *t, ws_info_t *info);
 
 /* performance knobs (no semantic effect) */

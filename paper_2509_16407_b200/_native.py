@@ -30,7 +30,7 @@ WS_F_INTERLEAVED = 16
 
 EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_erase", "ws_mixed",
            "ws_locate", "ws_probe_counts", "ws_occupied", "ws_export_items",
-           "ws_duplicate_scan", "ws_checksum", "ws_export_raw", "ws_info", "ws_tune",
+           "ws_duplicate_scan", "ws_checksum", "ws_export_raw", "ws_read_range", "ws_info", "ws_tune",
            "ws_partition", "ws_unpermute", "ws_xchg_create", "ws_xchg_handle", "ws_xchg_open",
            "ws_xchg_run", "ws_xchg_destroy", "ws_strerror")
 WS_TUNE_QUERY_ILP = 1
@@ -96,6 +96,7 @@ def load():
         lib.ws_duplicate_scan.argtypes = [vp, vp, vp, u64, C.POINTER(u64), vp]
         lib.ws_checksum.argtypes = [vp, C.POINTER(u64 * 4), vp]
         lib.ws_export_raw.argtypes = [vp, vp, u64, vp, vp]
+        lib.ws_read_range.argtypes = [vp, u64, u64, vp, u64, u64, vp, vp]
         lib.ws_info.argtypes = [vp, C.POINTER(WsInfo)]
         lib.ws_tune.argtypes = [vp, i32, i32]
         lib.ws_partition.argtypes = [vp, vp, vp, u64, u64, i32, vp, vp, vp, vp, vp, vp]

@@ -4,7 +4,7 @@ bench/adversarial.py).
 Every primary bucket b gets a blocker key X_b (pre-inserted) and a fresh key
 Y_b with the same primary bucket.  One mixed launch then runs, for every b,
 three concurrent actors -- erase(X_b), upsert(Y_b, 1, keep),
-upsert(Y_b, 2, keep) -- placed in different warps.  A table whose same-key
+upsert(Y_b, 2, keep) -- placed in adjacent warps of one CTA (actor_layout).  A table whose same-key
 writers are not externally synchronised can commit Y_b twice; the duplicate
 scan afterwards counts such buckets.  Device delay injection at the
 reference's hook stages (pre_reserve / pre_publish / pre_tombstone /
@@ -91,6 +91,32 @@ def generate_pairs(table, n_buckets: int, seed: int):
     return xs, ys
 
 
+def actor_layout(xs, ys, warp: int = 32):
+    """Op arrays of the three-actor script with the actors of a bucket
+    co-scheduled: buckets go in groups of `warp`; each group is three
+    consecutive warps of one launch -- erase(X) for the group's buckets, then
+    upsert(Y, 1, keep), then upsert(Y, 2, keep) -- so the three actors of
+    every bucket run in adjacent warps of the same CTA at the same time,
+    the device counterpart of the reference's three threads re-aligned by a
+    barrier every 128 buckets (bench/adversarial.py:37,169-177)."""
+    n = len(xs)
+    groups = (n + warp - 1) // warp
+    pad = groups * warp - n
+    role = np.repeat(np.arange(3, dtype=np.int64)[None, :], groups, axis=0)  # (groups, 3)
+    bucket = (np.arange(groups, dtype=np.int64)[:, None, None] * warp +
+              np.arange(warp, dtype=np.int64)[None, None, :])                 # (groups, 1, warp)
+    role = np.broadcast_to(role[:, :, None], (groups, 3, warp)).reshape(-1)
+    bucket = np.broadcast_to(bucket, (groups, 3, warp)).reshape(-1)
+    keep = bucket < n
+    role, bucket = role[keep], bucket[keep]
+    assert len(role) == 3 * n and pad >= 0
+    up = np.uint8(OP_UPSERT | (MERGE_KEEP << 4))
+    ops = np.where(role == 0, np.uint8(OP_ERASE), up).astype(np.uint8)
+    keys = np.where(role == 0, np.asarray(xs, np.uint64)[bucket], np.asarray(ys, np.uint64)[bucket])
+    vals = role.astype(np.uint64)  # erase 0, first upsert 1, second upsert 2
+    return ops, keys, vals
+
+
 def run_adversarial(design: str, buckets: int = 10_000, trials: int = 3, seed: int = 5,
                     profile: DelayProfile | None = None, device=None) -> dict:
     """`trials` replays over `buckets` primary buckets; returns total duplicate
@@ -110,10 +136,7 @@ def run_adversarial(design: str, buckets: int = 10_000, trials: int = 3, seed: i
         return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).to(dev).view(torch.uint64)
 
     n = buckets
-    ops = np.concatenate([np.full(n, OP_ERASE), np.full(n, OP_UPSERT | (MERGE_KEEP << 4)),
-                          np.full(n, OP_UPSERT | (MERGE_KEEP << 4))]).astype(np.uint8)
-    keys = np.concatenate([xs, ys, ys])
-    vals = np.concatenate([np.zeros(n, np.uint64), np.ones(n, np.uint64), np.full(n, 2, np.uint64)])
+    ops, keys, vals = actor_layout(xs, ys)
     d_ops = torch.from_numpy(ops).to(dev)
     d_keys, d_vals = cu(keys), cu(vals)
     per_trial = []

@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(AT, 1) k_bulk_apply(Dev d, const u64* __restri
                                                       const u32* __restrict__ I, const u32* __restrict__ goff, u64 G,
                                                       int gb_log2, int cap, int merge, u8* status, u32* dmask,
                                                       int gated) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   if (blockIdx.x >= G) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ApplySmem& S = *reinterpret_cast<ApplySmem*>(smem_raw);

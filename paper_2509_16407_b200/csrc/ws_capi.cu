@@ -10,7 +10,11 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <map>
+#include <mutex>
 #include <new>
+#include <shared_mutex>
 #include <thread>
 #include <vector>
 
@@ -24,7 +28,7 @@ using namespace ws;
 
 namespace {
 
-constexpr u32 N_STATE = 16;  // [0] tomb_ever [1] chain exhausted [2] bad keys [3] bad ops
+constexpr u32 N_STATE = 16;  // [0] tomb_ever; [8..11] the default per-call words (Dev::cs)
 
 Launchers launchers_for(int design) {
   switch (design) {
@@ -44,15 +48,15 @@ Launchers launchers_for(int design) {
 
 // mixed batches: count erase ops so the op kernel enables the concurrent-erase
 // (fenced tombstone-flag) path only when the batch really erases
-__global__ void k_count_erases(const u8* __restrict__ ops, u64 n, u32* state) {
+__global__ void k_count_erases(const u8* __restrict__ ops, u64 n, u32* cs) {
   u32 c = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
     c += (__ldg(ops + i) & 15) == OP_ERASE;
   c = __reduce_add_sync(0xFFFFFFFFu, c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(state + 4, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cs + 3, c);
 }
 
-__global__ void k_validate(const u64* __restrict__ keys, const u8* __restrict__ ops, u64 n, u32* state) {
+__global__ void k_validate(const u64* __restrict__ keys, const u8* __restrict__ ops, u64 n, u32* cs) {
   u32 bad_k = 0, bad_o = 0;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     bad_k += is_sentinel(__ldg(keys + i));
@@ -64,8 +68,8 @@ __global__ void k_validate(const u64* __restrict__ keys, const u8* __restrict__ 
   bad_k = __reduce_add_sync(0xFFFFFFFFu, bad_k);
   bad_o = __reduce_add_sync(0xFFFFFFFFu, bad_o);
   if ((threadIdx.x & 31) == 0) {
-    if (bad_k) atomicAdd(state + 2, bad_k);
-    if (bad_o) atomicAdd(state + 3, bad_o);
+    if (bad_k) atomicAdd(cs, bad_k);
+    if (bad_o) atomicAdd(cs + 1, bad_o);
   }
 }
 
@@ -147,11 +151,14 @@ struct ws_table {
   bool def_bs;
   u64 cell_words;
   u64 lock_words;
-  u64* h_pin;  // pinned scratch (64 words)
-  cudaStream_t s_aux, s_in;
-  cudaEvent_t ev_a, ev_b, ev_in;
-  std::vector<cudaEvent_t> ev_chunk;  // per-chunk H2D completion (staged mutations)
-  bool maybe_tomb;  // an erase may have run since creation / clear (host hint for the bulk path)
+  // Concurrent calls (reference tables/base.py:5-7: every public op may be
+  // called from many threads) hold `mu` shared for their whole host-side
+  // duration; only a chaining pool growth (which moves the node arena) takes
+  // it exclusively.  Per-call device state, pinned scratch and staging
+  // streams are private to the call / calling thread (CallCtx, pin(),
+  // staging()), so nothing else on the host side is shared.
+  std::shared_mutex mu;
+  std::atomic<bool> maybe_tomb;  // an erase may have run since creation / clear (host hint for the bulk path)
   int tune_bulk;    // WS_TUNE_BULK: 0 off, 1 auto, 2 always when eligible
   int tune_bulk_gb; // WS_TUNE_BULK_GROUP: buckets per group log2 (-1 = from the batch density)
 };
@@ -170,6 +177,59 @@ inline int cuda_err_at(cudaError_t e, int line) { return e == cudaSuccess ? WS_O
 #define WS_CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return note_cuda(e_, __LINE__); } while (0)
 
 inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+// pinned host scratch of the calling thread (64 words) for stream-ordered
+// device -> host reads of small results
+u64* pin() {
+  struct Pin {
+    u64* p = nullptr;
+    ~Pin() { if (p) cudaFreeHost(p); }
+  };
+  thread_local Pin tp;
+  if (!tp.p && cudaMallocHost((void**)&tp.p, 64 * 8) != cudaSuccess) tp.p = nullptr;
+  return tp.p;
+}
+
+// H2D / D2H staging streams and events of the calling thread on one device
+struct Staging {
+  cudaStream_t s_in = nullptr, s_aux = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_in = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;  // per-chunk H2D completion (staged mutations)
+  ~Staging() {
+    for (cudaEvent_t e : ev_chunk) cudaEventDestroy(e);
+    for (cudaEvent_t e : {ev_a, ev_b, ev_in}) if (e) cudaEventDestroy(e);
+    for (cudaStream_t x : {s_in, s_aux}) if (x) cudaStreamDestroy(x);
+  }
+};
+
+Staging* staging(int device) {
+  thread_local std::map<int, Staging> per_dev;
+  Staging& st = per_dev[device];
+  if (!st.s_in) {
+    if (cudaStreamCreateWithFlags(&st.s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&st.s_aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&st.ev_a, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&st.ev_b, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&st.ev_in, cudaEventDisableTiming) != cudaSuccess) {
+      per_dev.erase(device);
+      return nullptr;
+    }
+  }
+  return &st;
+}
+
+// One API call's private context: its 4 device state words (Dev::cs) and the
+// shared hold on the table it keeps for its host-side duration.
+struct CallCtx {
+  u32* cs;
+  std::shared_lock<std::shared_mutex>* lk;
+};
+
+inline Dev dev_of(const ws_table* t, const CallCtx& cx) {
+  Dev d = t->d;
+  d.cs = cx.cs;
+  return d;
+}
 
 bool is_device_ptr(const void* p) {
   if (!p) return true;
@@ -195,22 +255,28 @@ Mod make_mod(u64 d) {
 }
 
 // reset the invalid counters and count sentinel keys / bad op bytes
-int validate(ws_table* t, const u64* keys, const u8* ops, u64 n, cudaStream_t s, bool sync, u32 flags) {
+int validate(const u64* keys, const u8* ops, u64 n, cudaStream_t s, bool sync, u32 flags, const CallCtx& cx) {
   if (flags & WS_F_NO_CHECK) return WS_OK;
-  WS_CK(cudaMemsetAsync(t->d.state + 2, 0, 2 * sizeof(u32), s));
-  if (n) k_validate<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(keys, ops, n, t->d.state);
+  WS_CK(cudaMemsetAsync(cx.cs, 0, 2 * sizeof(u32), s));
+  if (n) k_validate<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(keys, ops, n, cx.cs);
   WS_CK(cudaGetLastError());
   if (!sync) return WS_OK;
-  WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 2, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  u64* hp = pin();
+  if (!hp) return WS_ERR_ALLOC;
+  WS_CK(cudaMemcpyAsync(hp, cx.cs, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
   WS_CK(cudaStreamSynchronize(s));
-  const u32* c = (const u32*)t->h_pin;
+  const u32* c = (const u32*)hp;
   if (c[0]) return WS_ERR_INVALID_KEY;
   if (c[1]) return WS_ERR_INVALID_OP;
   return WS_OK;
 }
 
-// chaining: grow the node pool by 1.5x when a launch exhausted it
+// chaining: grow the node pool by 1.5x when a launch exhausted it.  The
+// caller holds the table exclusively; every launch that may still read the
+// old arena (other threads' calls return before their kernels finish) is
+// drained by a device synchronisation before the arena moves.
 int chain_grow(ws_table* t, cudaStream_t s) {
+  WS_CK(cudaDeviceSynchronize());
   const u64 old = t->d.chain_cap;
   const u64 ncap = old + std::max<u64>(old / 2, 64);
   const u64 words = ncap * (u64)t->d.wpn;
@@ -223,11 +289,12 @@ int chain_grow(ws_table* t, cudaStream_t s) {
   t->d.chain_cap = ncap;
   t->cell_words = words;
   // every index < old was handed out; failed bumps overshot past it
-  WS_CK(cudaMemcpyAsync(t->h_pin, t->d.chain_next, 8, cudaMemcpyDeviceToHost, s));
+  u64* hp = pin();
+  if (!hp) return WS_ERR_ALLOC;
+  WS_CK(cudaMemcpyAsync(hp, t->d.chain_next, 8, cudaMemcpyDeviceToHost, s));
   WS_CK(cudaStreamSynchronize(s));
-  if (t->h_pin[0] > old) t->h_pin[0] = old;
-  WS_CK(cudaMemcpyAsync(t->d.chain_next, t->h_pin, 8, cudaMemcpyHostToDevice, s));
-  WS_CK(cudaMemsetAsync(t->d.state + 1, 0, sizeof(u32), s));
+  if (hp[0] > old) hp[0] = old;
+  WS_CK(cudaMemcpyAsync(t->d.chain_next, hp, 8, cudaMemcpyHostToDevice, s));
   WS_CK(cudaStreamSynchronize(s));
   return WS_OK;
 }
@@ -243,10 +310,11 @@ bool bulk_eligible(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n,
   if (n >= (1ull << 32) || !bulk_aligned(keys, vals)) return false;
   if (t->tune_bulk == 1 && (n < (1ull << 20) || n < 4 * t->d.nb)) return false;
   if (t->maybe_tomb) {  // an erase ran: ask the device whether it ever tombstoned
-    if (cudaMemcpyAsync(t->h_pin, t->d.state, sizeof(u32), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+    u64* hp = pin();
+    if (!hp || cudaMemcpyAsync(hp, t->d.state, sizeof(u32), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
         cudaStreamSynchronize(s) != cudaSuccess)
       return false;
-    if (*(const u32*)t->h_pin) return false;
+    if (*(const u32*)hp) return false;
     t->maybe_tomb = false;
   }
   return true;
@@ -277,7 +345,7 @@ __global__ void k_kind_scatter(const u32* __restrict__ perm, const u8* __restric
 
 int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
-                     bool query_only);
+                     bool query_only, const CallCtx& cx);
 
 // first index of every op-byte value in the sorted op array (~0 when absent)
 __global__ void k_seg_starts(const u8* __restrict__ op_sorted, u64 n, u64* start) {
@@ -296,8 +364,8 @@ __global__ void k_seg_starts(const u8* __restrict__ op_sorted, u64 n, u64* start
 // stream, then the results are scattered back.  Running the segments in
 // sequence is one serial order of the concurrent batch.
 int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
-                       u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert) {
-  int rc = validate(t, keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags);
+                       u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, const CallCtx& cx) {
+  int rc = validate(keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
   if (rc) return rc;
   u8 *op_p = nullptr, *st_p = nullptr;
   u32 *idx = nullptr, *perm = nullptr;
@@ -336,17 +404,19 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
     const int kind = v & 15, merge = v >> 4;
     const u64 m = hi - lo;
     if (kind == OP_UPSERT && merge <= M_MIN && v_p) {
-      rc = run_device_plain(t, nullptr, v, k_p + lo, v_p + lo, m, st_p + lo, nullptr, s, inner, false, true, false);
+      rc = run_device_plain(t, nullptr, v, k_p + lo, v_p + lo, m, st_p + lo, nullptr, s, inner, false, true, false,
+                            cx);
       if (vo_p && !rc) rc = cuda_err(cudaMemsetAsync(vo_p + lo, 0, 8 * m, s));
     } else if (kind == OP_ERASE && merge == 0) {
-      rc = run_device_plain(t, nullptr, v, k_p + lo, nullptr, m, st_p + lo, nullptr, s, inner, true, false, false);
+      rc = run_device_plain(t, nullptr, v, k_p + lo, nullptr, m, st_p + lo, nullptr, s, inner, true, false, false,
+                            cx);
       if (vo_p && !rc) rc = cuda_err(cudaMemsetAsync(vo_p + lo, 0, 8 * m, s));
     } else if (kind == OP_QUERY && merge == 0) {
       rc = run_device_plain(t, nullptr, v, k_p + lo, nullptr, m, st_p + lo, vo_p ? vo_p + lo : nullptr, s, inner,
-                            false, false, true);
+                            false, false, true, cx);
     } else {  // value-less upserts or invalid op bytes (gated): the generic kernel handles them
       rc = run_device_plain(t, op_p + lo, 0, k_p + lo, v_p ? v_p + lo : nullptr, m, st_p + lo,
-                            vo_p ? vo_p + lo : nullptr, s, inner, has_erase, has_upsert, false);
+                            vo_p ? vo_p + lo : nullptr, s, inner, has_erase, has_upsert, false, cx);
     }
   }
   if (!rc) {
@@ -361,12 +431,12 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
 
 int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
-                     bool query_only) {
+                     bool query_only, const CallCtx& cx) {
   if (ops && !query_only && n >= (1u << 16) && n < (1ull << 32) && !t->d.delay_ns &&
       !(flags & (WS_F_SERIAL | WS_F_INTERLEAVED | kF_NO_KIND_SORT)))
-    return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert);
+    return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, cx);
   const bool sync = (flags & WS_F_SYNC_CHECK) != 0;
-  int rc = validate(t, keys, ops, n, s, sync, flags);
+  int rc = validate(keys, ops, n, s, sync, flags, cx);
   if (rc) return rc;
   if (!n) return WS_OK;
   const int gated = (flags & kF_VALIDATED) ? 1 : (flags & WS_F_NO_CHECK) ? 0 : 1;
@@ -375,17 +445,17 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
     BulkPlan plan = bulk_plan(n, t->d.nb, t->tune_bulk_gb);
     plan.skip_b = t->tune_bulk == 3;
     plan.cap = std::max(0, t->d.shortcut - 4);
-    return cuda_err(bulk_upsert_p2md(t->d, keys, vals, n, uop >> 4, status, gated, s, plan));
+    return cuda_err(bulk_upsert_p2md(dev_of(t, cx), keys, vals, n, uop >> 4, status, gated, s, plan));
   }
   int conc = (has_erase || t->cfg.multi_stream) ? 1 : 0;
   if (ops && !t->cfg.multi_stream && !(flags & WS_F_SERIAL)) {
     // let the device decide: conc_erase = 2 reads the erase count at launch
-    WS_CK(cudaMemsetAsync(t->d.state + 4, 0, sizeof(u32), s));
-    k_count_erases<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(ops, n, t->d.state);
+    WS_CK(cudaMemsetAsync(cx.cs + 3, 0, sizeof(u32), s));
+    k_count_erases<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(ops, n, cx.cs);
     conc = 2;
   }
   if (query_only && !(flags & WS_F_SERIAL)) {
-    QueryArgs qa{t->d, keys, n, vout, status, conc, gated, t->cfg.phased ? 1 : 0, s};
+    QueryArgs qa{dev_of(t, cx), keys, n, vout, status, conc, gated, t->cfg.phased ? 1 : 0, s};
     t->L.query(qa, t->def_bs);
     return cuda_err(cudaGetLastError());
   }
@@ -394,18 +464,30 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
   if (chain_up && !st) {  // the grow-and-redo protocol needs per-op statuses
     WS_CK(cudaMallocAsync((void**)&st, n, s));
   }
-  OpsArgs lo{t->d, ops, uop, keys, vals, n, st, vout, nullptr, nullptr, nullptr, conc, gated, 0,
+  if (chain_up) WS_CK(cudaMemsetAsync(cx.cs + 2, 0, sizeof(u32), s));
+  OpsArgs lo{dev_of(t, cx), ops, uop, keys, vals, n, st, vout, nullptr, nullptr, nullptr, conc, gated, 0,
              (flags & WS_F_SERIAL) ? 1 : 0, s};
   t->L.ops(lo, t->def_bs);
   rc = cuda_err(cudaGetLastError());
   while (rc == WS_OK && chain_up) {
-    WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 1, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    u64* hp = pin();
+    if (!hp) { rc = WS_ERR_ALLOC; break; }
+    WS_CK(cudaMemcpyAsync(hp, cx.cs + 2, sizeof(u32), cudaMemcpyDeviceToHost, s));
     WS_CK(cudaStreamSynchronize(s));
-    if (!*(const u32*)t->h_pin) break;
-    rc = chain_grow(t, s);
+    if (!*(const u32*)hp) break;
+    // the pool is exhausted: grow it exclusively (unless a concurrent call
+    // already did), then redo this launch's deferred ops
+    const u64 seen = lo.d.chain_cap;
+    cx.lk->unlock();
+    {
+      std::unique_lock<std::shared_mutex> ex(t->mu);
+      if (t->d.chain_cap == seen) rc = chain_grow(t, s);
+    }
+    cx.lk->lock();
     if (rc) break;
+    WS_CK(cudaMemsetAsync(cx.cs + 2, 0, sizeof(u32), s));
     lo.redo = st;
-    lo.d = t->d;  // the pool moved
+    lo.d = dev_of(t, cx);  // the pool moved
     t->L.ops(lo, t->def_bs);
     rc = cuda_err(cudaGetLastError());
   }
@@ -454,7 +536,12 @@ __global__ void k_upsert_range(const u8* op_sorted, u64 n, u32* lohi) {
     if (first) atomicMin(lohi, (u32)j);
     if (last) atomicMax(lohi + 1, (u32)(j + 1));
     const int m = op_sorted[j] >> 4;
-    if (first && m != M_ADD && m != M_MAX && m != M_MIN) atomicOr(lohi + 2, 1u);  // order-sensitive merge
+    // any upsert with an order-sensitive merge (REPLACE / KEEP) rules out the
+    // hash sort for the whole span; warp-aggregated, one atomic per warp
+    const bool ord = up && m != M_ADD && m != M_MAX && m != M_MIN;
+    const unsigned am = __activemask();
+    const unsigned any = __ballot_sync(am, ord);
+    if (any && (threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) atomicOr(lohi + 2, 1u);
   }
 }
 
@@ -503,13 +590,18 @@ __global__ void k_comb_expand(const u32* si, const u32* head, const u32* seg, u6
 
 int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
-               bool query_only) {
+               bool query_only, const CallCtx& cx) {
   if (!(flags & WS_F_COMBINE) || query_only || !has_upsert || n < 2 || n >= (1ull << 32) ||
       (flags & WS_F_SERIAL))
     return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s, flags & ~WS_F_COMBINE, has_erase,
-                            has_upsert, query_only);
-  int rc = validate(t, keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags);
+                            has_upsert, query_only, cx);
+  int rc = validate(keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
   if (rc) return rc;
+  // the folded batch keeps the kernels gated on this call's validation verdict
+  // (an asynchronous check is not read back here, but a batch holding a
+  // sentinel key or a bad op byte still mutates nothing)
+  const u32 inner = (flags & ~(WS_F_COMBINE | WS_F_SYNC_CHECK)) | WS_F_NO_CHECK |
+                    ((flags & WS_F_NO_CHECK) ? 0u : kF_VALIDATED);
   // scratch: sorted keys / indices, heads, segment ids, op-values, groups
   u64 *sk = nullptr, *gkey = nullptr, *gval = nullptr, *gvo = nullptr;
   u32 *idx = nullptr, *si = nullptr, *head = nullptr, *seg = nullptr, *uniq = nullptr;
@@ -559,9 +651,11 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
     WS_CK(cudaMemsetAsync(lohi, 0xFF, 4, s));
     WS_CK(cudaMemsetAsync(lohi + 1, 0, 8, s));
     k_upsert_range<<<grid_for(n), kThreads, 0, s>>>(op_sorted, n, lohi);
-    WS_CK(cudaMemcpyAsync(t->h_pin, lohi, 12, cudaMemcpyDeviceToHost, s));
+    u64* hp = pin();
+    if (!hp) return WS_ERR_ALLOC;
+    WS_CK(cudaMemcpyAsync(hp, lohi, 12, cudaMemcpyDeviceToHost, s));
     WS_CK(cudaStreamSynchronize(s));
-    const u32* hl = (const u32*)t->h_pin;
+    const u32* hl = (const u32*)hp;
     lo = hl[0] == 0xFFFFFFFFu ? 0 : hl[0];
     hi = hl[0] == 0xFFFFFFFFu ? 0 : hl[1];
     span_commutative = hl[2] == 0;
@@ -570,9 +664,7 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
       for (void* p : {(void*)sk, (void*)idx, (void*)si, (void*)head, (void*)seg, (void*)uniq, (void*)ov,
                       (void*)agg, (void*)nruns, tmp, (void*)op_sorted, (void*)keys_by_op})
         if (p) cudaFreeAsync(p, s);
-      return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s,
-                              (flags & ~(WS_F_COMBINE | WS_F_SYNC_CHECK)) | WS_F_NO_CHECK, has_erase, has_upsert,
-                              false);
+      return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s, inner, has_erase, has_upsert, false, cx);
     }
     if (lo > 0) {
       WS_CK(cudaMemcpyAsync(sk, keys_by_op, 8 * lo, cudaMemcpyDeviceToDevice, s));
@@ -611,9 +703,11 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   k_comb_heads<<<grid_for(n), kThreads, 0, s>>>(sk, si, ops, uop, vals, n, head, ov);
   cub::DeviceScan::InclusiveSum(tmp, tb2, head, seg, (int64_t)n, s);
   cub::DeviceReduce::ReduceByKey(tmp, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
-  WS_CK(cudaMemcpyAsync(t->h_pin, nruns, 8, cudaMemcpyDeviceToHost, s));
+  u64* hp = pin();
+  if (!hp) return WS_ERR_ALLOC;
+  WS_CK(cudaMemcpyAsync(hp, nruns, 8, cudaMemcpyDeviceToHost, s));
   WS_CK(cudaStreamSynchronize(s));
-  const u64 ng = t->h_pin[0];
+  const u64 ng = hp[0];
   WS_CK(cudaMallocAsync((void**)&gkey, 8 * ng, s));
   WS_CK(cudaMallocAsync((void**)&gval, 8 * ng, s));
   WS_CK(cudaMallocAsync((void**)&gvo, 8 * ng, s));
@@ -622,8 +716,8 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   k_comb_groups<<<grid_for(n), kThreads, 0, s>>>(sk, si, head, seg, ops, uop, n, gkey, gop);
   k_comb_vals<<<grid_for(ng), kThreads, 0, s>>>(agg, ng, gval);
   WS_CK(cudaGetLastError());
-  rc = run_device_plain(t, ops ? gop : nullptr, uop, gkey, vals ? gval : nullptr, ng, gst, gvo, s,
-                        (flags & ~(WS_F_COMBINE | WS_F_SYNC_CHECK)) | WS_F_NO_CHECK, has_erase, has_upsert, false);
+  rc = run_device_plain(t, ops ? gop : nullptr, uop, gkey, vals ? gval : nullptr, ng, gst, gvo, s, inner, has_erase,
+                        has_upsert, false, cx);
   if (!rc) {
     k_comb_expand<<<grid_for(n), kThreads, 0, s>>>(si, head, seg, n, gst, gvo, status, vout);
     rc = cuda_err(cudaGetLastError());
@@ -681,8 +775,11 @@ int host_validate(const u64* keys, const u8* ops, u64 n) {
 
 int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
-               bool query_only) {
+               bool query_only, const CallCtx& cx) {
   if (!n) return WS_OK;
+  Staging* sg = staging(t->device);
+  u64* hp = pin();
+  if (!sg || !hp) return WS_ERR_ALLOC;
   const bool k_dev = is_device_ptr(keys), v_dev = is_device_ptr(vals), o_dev = is_device_ptr(ops);
   const bool st_dev = is_device_ptr(status), vo_dev = is_device_ptr(vout);
   const bool hk = !k_dev, hv = vals && !v_dev, ho = ops && !o_dev;
@@ -698,36 +795,36 @@ int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   u8* dst = hst ? (u8*)carve(n) : status;
   u64* dvo = hvo ? (u64*)carve(8 * n) : vout;
   const bool check = !(flags & WS_F_NO_CHECK);
-  if (check) WS_CK(cudaMemsetAsync(t->d.state + 2, 0, 2 * sizeof(u32), s));
-  WS_CK(cudaEventRecord(t->ev_b, s));  // staging allocation visible to s_in / s_aux
-  WS_CK(cudaStreamWaitEvent(t->s_in, t->ev_b, 0));
-  WS_CK(cudaStreamWaitEvent(t->s_aux, t->ev_b, 0));
+  if (check) WS_CK(cudaMemsetAsync(cx.cs, 0, 2 * sizeof(u32), s));
+  WS_CK(cudaEventRecord(sg->ev_b, s));  // staging allocation visible to s_in / s_aux
+  WS_CK(cudaStreamWaitEvent(sg->s_in, sg->ev_b, 0));
+  WS_CK(cudaStreamWaitEvent(sg->s_aux, sg->ev_b, 0));
   const bool chain_up = t->cfg.design == D_CHAINING && has_upsert;
   const u64 chunk = chain_up ? n : (u64)1 << 22;
   const u32 sub = WS_F_NO_CHECK | (flags & (WS_F_SERIAL | WS_F_COMBINE));
   int rc = WS_OK;
   auto h2d = [&](u64 off, u64 m) -> int {
-    if (hk) WS_CK(cudaMemcpyAsync((void*)(dk + off), keys + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
-    if (hv) WS_CK(cudaMemcpyAsync((void*)(dv + off), vals + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
-    if (ho) WS_CK(cudaMemcpyAsync((void*)(dops + off), ops + off, m, cudaMemcpyHostToDevice, t->s_in));
-    WS_CK(cudaEventRecord(t->ev_in, t->s_in));
-    WS_CK(cudaStreamWaitEvent(s, t->ev_in, 0));
+    if (hk) WS_CK(cudaMemcpyAsync((void*)(dk + off), keys + off, 8 * m, cudaMemcpyHostToDevice, sg->s_in));
+    if (hv) WS_CK(cudaMemcpyAsync((void*)(dv + off), vals + off, 8 * m, cudaMemcpyHostToDevice, sg->s_in));
+    if (ho) WS_CK(cudaMemcpyAsync((void*)(dops + off), ops + off, m, cudaMemcpyHostToDevice, sg->s_in));
+    WS_CK(cudaEventRecord(sg->ev_in, sg->s_in));
+    WS_CK(cudaStreamWaitEvent(s, sg->ev_in, 0));
     if (check) k_validate<<<grid_for(m, kThreads, 4), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
-                                                                         t->d.state);
+                                                                         cx.cs);
     return cuda_err(cudaGetLastError());
   };
   auto d2h = [&](u64 off, u64 m) -> int {
     if (!hst && !hvo) return WS_OK;
-    WS_CK(cudaEventRecord(t->ev_a, s));
-    WS_CK(cudaStreamWaitEvent(t->s_aux, t->ev_a, 0));
-    if (hst) WS_CK(cudaMemcpyAsync(status + off, dst + off, m, cudaMemcpyDeviceToHost, t->s_aux));
-    if (hvo) WS_CK(cudaMemcpyAsync(vout + off, dvo + off, 8 * m, cudaMemcpyDeviceToHost, t->s_aux));
+    WS_CK(cudaEventRecord(sg->ev_a, s));
+    WS_CK(cudaStreamWaitEvent(sg->s_aux, sg->ev_a, 0));
+    if (hst) WS_CK(cudaMemcpyAsync(status + off, dst + off, m, cudaMemcpyDeviceToHost, sg->s_aux));
+    if (hvo) WS_CK(cudaMemcpyAsync(vout + off, dvo + off, 8 * m, cudaMemcpyDeviceToHost, sg->s_aux));
     return WS_OK;
   };
   auto compute = [&](u64 off, u64 m) -> int {
     return run_device(t, dops ? dops + off : nullptr, uop, dk + off, dv ? dv + off : nullptr, m,
                       dst ? dst + off : nullptr, dvo ? dvo + off : nullptr, s, sub, has_erase, has_upsert,
-                      query_only);
+                      query_only, cx);
   };
   if (query_only) {
     for (u64 off = 0; off < n && rc == WS_OK; off += chunk) {
@@ -743,50 +840,50 @@ int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
     // the copy engine streams them in; each chunk's compute then starts as
     // soon as its own copy lands, so the kernels hide under the H2D stream.
     const u64 nch = (n + chunk - 1) / chunk;
-    while (t->ev_chunk.size() < nch) {
+    while (sg->ev_chunk.size() < nch) {
       cudaEvent_t e;
       WS_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      t->ev_chunk.push_back(e);
+      sg->ev_chunk.push_back(e);
     }
     for (u64 c = 0; c < nch; c++) {
       const u64 off = c * chunk, m = std::min(chunk, n - off);
-      if (hk) WS_CK(cudaMemcpyAsync((void*)(dk + off), keys + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
-      if (hv) WS_CK(cudaMemcpyAsync((void*)(dv + off), vals + off, 8 * m, cudaMemcpyHostToDevice, t->s_in));
-      if (ho) WS_CK(cudaMemcpyAsync((void*)(dops + off), ops + off, m, cudaMemcpyHostToDevice, t->s_in));
-      WS_CK(cudaEventRecord(t->ev_chunk[c], t->s_in));
+      if (hk) WS_CK(cudaMemcpyAsync((void*)(dk + off), keys + off, 8 * m, cudaMemcpyHostToDevice, sg->s_in));
+      if (hv) WS_CK(cudaMemcpyAsync((void*)(dv + off), vals + off, 8 * m, cudaMemcpyHostToDevice, sg->s_in));
+      if (ho) WS_CK(cudaMemcpyAsync((void*)(dops + off), ops + off, m, cudaMemcpyHostToDevice, sg->s_in));
+      WS_CK(cudaEventRecord(sg->ev_chunk[c], sg->s_in));
     }
     if (check && hk && (!ops || ho)) {
       rc = host_validate(keys, ho ? ops : nullptr, n);
     } else if (check) {
       for (u64 c = 0; c < nch; c++) {
         const u64 off = c * chunk, m = std::min(chunk, n - off);
-        WS_CK(cudaStreamWaitEvent(s, t->ev_chunk[c], 0));
+        WS_CK(cudaStreamWaitEvent(s, sg->ev_chunk[c], 0));
         k_validate<<<grid_for(m, kThreads, 4), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
-                                                                 t->d.state);
+                                                                 cx.cs);
       }
       WS_CK(cudaGetLastError());
-      WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 2, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      WS_CK(cudaMemcpyAsync(hp, cx.cs, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
       WS_CK(cudaStreamSynchronize(s));
-      const u32* c = (const u32*)t->h_pin;
+      const u32* c = (const u32*)hp;
       if (c[0]) rc = WS_ERR_INVALID_KEY;
       else if (c[1]) rc = WS_ERR_INVALID_OP;
     }
     for (u64 c = 0; c < nch && rc == WS_OK; c++) {
       const u64 off = c * chunk, m = std::min(chunk, n - off);
-      WS_CK(cudaStreamWaitEvent(s, t->ev_chunk[c], 0));
+      WS_CK(cudaStreamWaitEvent(s, sg->ev_chunk[c], 0));
       rc = compute(off, m);
       if (!rc) rc = d2h(off, m);
     }
   }
-  WS_CK(cudaEventRecord(t->ev_b, t->s_aux));
-  WS_CK(cudaStreamWaitEvent(s, t->ev_b, 0));
-  WS_CK(cudaEventRecord(t->ev_in, t->s_in));
-  WS_CK(cudaStreamWaitEvent(s, t->ev_in, 0));
+  WS_CK(cudaEventRecord(sg->ev_b, sg->s_aux));
+  WS_CK(cudaStreamWaitEvent(s, sg->ev_b, 0));
+  WS_CK(cudaEventRecord(sg->ev_in, sg->s_in));
+  WS_CK(cudaStreamWaitEvent(s, sg->ev_in, 0));
   cudaFreeAsync(buf, s);
   if (query_only && check && rc == WS_OK) {
-    WS_CK(cudaMemcpyAsync(t->h_pin, t->d.state + 2, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    WS_CK(cudaMemcpyAsync(hp, cx.cs, 2 * sizeof(u32), cudaMemcpyDeviceToHost, s));
     WS_CK(cudaStreamSynchronize(s));
-    const u32* c = (const u32*)t->h_pin;
+    const u32* c = (const u32*)hp;
     if (c[0]) rc = WS_ERR_INVALID_KEY;
   }
   WS_CK(cudaStreamSynchronize(s));
@@ -802,9 +899,16 @@ int run_batch(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* va
   cudaStream_t s = S(stream);
   const bool all_dev = is_device_ptr(keys) && is_device_ptr(vals) && is_device_ptr(ops) &&
                        is_device_ptr(status) && is_device_ptr(vout);
-  if (all_dev)
-    return run_device(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only);
-  return run_staged(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only);
+  std::shared_lock<std::shared_mutex> lk(t->mu);
+  CallCtx cx{nullptr, &lk};
+  WS_CK(cudaMallocAsync((void**)&cx.cs, 4 * sizeof(u32), s));
+  int rc = cuda_err(cudaMemsetAsync(cx.cs, 0, 4 * sizeof(u32), s));
+  if (!rc)
+    rc = all_dev ? run_device(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only, cx)
+                 : run_staged(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only,
+                              cx);
+  cudaFreeAsync(cx.cs, s);
+  return rc;
 }
 
 u64 npairs_of(const ws_table* t) { return t->cell_words / 2; }
@@ -812,9 +916,11 @@ u64 npairs_of(const ws_table* t) { return t->cell_words / 2; }
 int next_node_of(ws_table* t, cudaStream_t s, u64& nn) {
   nn = 0;
   if (t->cfg.design != D_CHAINING) return WS_OK;
-  WS_CK(cudaMemcpyAsync(t->h_pin, t->d.chain_next, 8, cudaMemcpyDeviceToHost, s));
+  u64* hp = pin();
+  if (!hp) return WS_ERR_ALLOC;
+  WS_CK(cudaMemcpyAsync(hp, t->d.chain_next, 8, cudaMemcpyDeviceToHost, s));
   WS_CK(cudaStreamSynchronize(s));
-  nn = t->h_pin[0];
+  nn = hp[0];
   if (nn > t->d.chain_cap) nn = t->d.chain_cap;
   return WS_OK;
 }
@@ -838,12 +944,14 @@ int compact_items(ws_table* t, cudaStream_t s, ulonglong2** out, u64* count) {
   void* tmp = nullptr;
   WS_CK(cudaMallocAsync(&tmp, tmp_bytes + 16, s));
   cub::DeviceSelect::Flagged(tmp, tmp_bytes, in, flags, sel, nsel, (int64_t)np, s);
-  WS_CK(cudaMemcpyAsync(t->h_pin, nsel, 8, cudaMemcpyDeviceToHost, s));
+  u64* hp = pin();
+  if (!hp) return WS_ERR_ALLOC;
+  WS_CK(cudaMemcpyAsync(hp, nsel, 8, cudaMemcpyDeviceToHost, s));
   cudaFreeAsync(tmp, s);
   cudaFreeAsync(flags, s);
   cudaFreeAsync(nsel, s);
   WS_CK(cudaStreamSynchronize(s));
-  *count = t->h_pin[0];
+  *count = hp[0];
   *out = sel;
   return cuda_err(cudaGetLastError());
 }
@@ -854,7 +962,13 @@ int compact_items(ws_table* t, cudaStream_t s, ulonglong2** out, u64* count) {
 int ws_internal_run(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
                     u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, bool query_only) {
   if (cudaSetDevice(t->device) != cudaSuccess) return WS_ERR_CUDA;
-  return run_device(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only);
+  std::shared_lock<std::shared_mutex> lk(t->mu);
+  CallCtx cx{nullptr, &lk};
+  WS_CK(cudaMallocAsync((void**)&cx.cs, 4 * sizeof(u32), s));
+  int rc = cuda_err(cudaMemsetAsync(cx.cs, 0, 4 * sizeof(u32), s));
+  if (!rc) rc = run_device(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only, cx);
+  cudaFreeAsync(cx.cs, s);
+  return rc;
 }
 int ws_internal_device(ws_table* t) { return t->device; }
 
@@ -948,6 +1062,7 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   if (cudaMemset(d.locks, 0, t->lock_words * 4) != cudaSuccess) return fail(WS_ERR_CUDA);
   if (cudaMalloc((void**)&d.state, N_STATE * 4) != cudaSuccess) return fail(WS_ERR_ALLOC);
   if (cudaMemset(d.state, 0, N_STATE * 4) != cudaSuccess) return fail(WS_ERR_CUDA);
+  d.cs = d.state + 8;  // only internal launches outside any API call use the default words
   if (c.design == D_CHAINING) {
     const u64 nn = nb + 1;
     if (cudaMemcpy(d.chain_next, &nn, 8, cudaMemcpyHostToDevice) != cudaSuccess) return fail(WS_ERR_CUDA);
@@ -967,10 +1082,6 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
     if (cudaMalloc((void**)&d.bfs_busy, 4 * d.n_bfs) != cudaSuccess) return fail(WS_ERR_ALLOC);
     if (cudaMemset(d.bfs_busy, 0, 4 * d.n_bfs) != cudaSuccess) return fail(WS_ERR_CUDA);
   }
-  if (cudaMallocHost((void**)&t->h_pin, 64 * 8) != cudaSuccess) return fail(WS_ERR_ALLOC);
-  if (cudaStreamCreateWithFlags(&t->s_aux, cudaStreamNonBlocking) != cudaSuccess) return fail(WS_ERR_CUDA);
-  if (cudaStreamCreateWithFlags(&t->s_in, cudaStreamNonBlocking) != cudaSuccess) return fail(WS_ERR_CUDA);
-  if (cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
   {
     // keep staging / scratch allocations of the stream-ordered pool mapped
     // between calls instead of returning them to the driver at every sync
@@ -980,8 +1091,6 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
-  if (cudaEventCreateWithFlags(&t->ev_a, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
-  if (cudaEventCreateWithFlags(&t->ev_b, cudaEventDisableTiming) != cudaSuccess) return fail(WS_ERR_CUDA);
   t->L.preload(t->def_bs);
   preload_fn(k_validate);
   preload_fn(k_checksum);
@@ -1003,13 +1112,6 @@ int ws_destroy(ws_table* t) {
   if (d.chain_next) cudaFree(d.chain_next);
   if (d.bfs_mem) cudaFree(d.bfs_mem);
   if (d.bfs_busy) cudaFree(d.bfs_busy);
-  if (t->h_pin) cudaFreeHost(t->h_pin);
-  if (t->s_aux) cudaStreamDestroy(t->s_aux);
-  if (t->s_in) cudaStreamDestroy(t->s_in);
-  if (t->ev_in) cudaEventDestroy(t->ev_in);
-  for (cudaEvent_t e : t->ev_chunk) cudaEventDestroy(e);
-  if (t->ev_a) cudaEventDestroy(t->ev_a);
-  if (t->ev_b) cudaEventDestroy(t->ev_b);
   delete t;
   return WS_OK;
 }
@@ -1025,8 +1127,10 @@ int ws_clear(ws_table* t, void* stream) {
   WS_CK(cudaMemsetAsync(d.state, 0, N_STATE * 4, s));
   t->maybe_tomb = false;
   if (t->cfg.design == D_CHAINING) {
-    t->h_pin[0] = d.nb + 1;
-    WS_CK(cudaMemcpyAsync(d.chain_next, t->h_pin, 8, cudaMemcpyHostToDevice, s));
+    u64* hp = pin();
+    if (!hp) return WS_ERR_ALLOC;
+    hp[0] = d.nb + 1;
+    WS_CK(cudaMemcpyAsync(d.chain_next, hp, 8, cudaMemcpyHostToDevice, s));
     WS_CK(cudaStreamSynchronize(s));
   }
   return WS_OK;
@@ -1088,7 +1192,7 @@ int ws_probe_counts(ws_table* t, const uint8_t* ops, const uint64_t* keys, const
   if (!n) { if (lock_touches) *lock_touches = 0; return WS_OK; }
   // stage everything (instrumented runs are measurement passes, not hot)
   char* buf = nullptr;
-  const u64 need = n * (1 + 8 + 8 + 1 + 8 + 4) + 1024;
+  const u64 need = n * (1 + 8 + 8 + 1 + 8 + 4) + 2048;
   WS_CK(cudaMallocAsync((void**)&buf, need, s));
   char* p = buf;
   auto carve = [&](u64 bytes) { char* r = p; p += (bytes + 127) & ~127ull; return r; };
@@ -1104,19 +1208,25 @@ int ws_probe_counts(ws_table* t, const uint8_t* ops, const uint64_t* keys, const
   if (vals) WS_CK(cudaMemcpyAsync(dv, vals, 8 * n, cudaMemcpyDefault, s));
   else WS_CK(cudaMemsetAsync(dv, 0, 8 * n, s));
   WS_CK(cudaMemsetAsync(dlock, 0, 8, s));
-  int rc = validate(t, dk, dops, n, s, true, 0);
+  u32* cs = (u32*)carve(16);
+  WS_CK(cudaMemsetAsync(cs, 0, 16, s));
+  std::shared_lock<std::shared_mutex> lk(t->mu);
+  const CallCtx cx{cs, &lk};
+  u64* hp = pin();
+  if (!hp) { cudaFreeAsync(buf, s); cudaStreamSynchronize(s); return WS_ERR_ALLOC; }
+  int rc = validate(dk, dops, n, s, true, 0, cx);
   if (rc) { cudaFreeAsync(buf, s); cudaStreamSynchronize(s); return rc; }
-  OpsArgs lo{t->d, dops, 0, dk, dv, n, dst, dvo, nullptr, dpr, dlock, 1, 0, 1,
+  OpsArgs lo{dev_of(t, cx), dops, 0, dk, dv, n, dst, dvo, nullptr, dpr, dlock, 1, 0, 1,
              (flags & WS_F_SERIAL) ? 1 : 0, s};
   t->L.ops(lo, t->def_bs);
   rc = cuda_err(cudaGetLastError());
   if (!rc && status) WS_CK(cudaMemcpyAsync(status, dst, n, cudaMemcpyDefault, s));
   if (!rc && vals_out) WS_CK(cudaMemcpyAsync(vals_out, dvo, 8 * n, cudaMemcpyDefault, s));
   if (!rc) WS_CK(cudaMemcpyAsync(probes, dpr, 4 * n, cudaMemcpyDefault, s));
-  if (!rc) WS_CK(cudaMemcpyAsync(t->h_pin, dlock, 8, cudaMemcpyDeviceToHost, s));
+  if (!rc) WS_CK(cudaMemcpyAsync(hp, dlock, 8, cudaMemcpyDeviceToHost, s));
   cudaFreeAsync(buf, s);
   WS_CK(cudaStreamSynchronize(s));
-  if (!rc && lock_touches) *lock_touches = t->h_pin[0];
+  if (!rc && lock_touches) *lock_touches = hp[0];
   return rc;
 }
 
@@ -1139,10 +1249,12 @@ int ws_checksum(ws_table* t, uint64_t out[4], void* stream) {
   WS_CK(cudaMemsetAsync(dout, 0, 32, s));
   const u64 np = npairs_of(t);
   k_checksum<<<grid_for(np), kThreads, 0, s>>>(t->d, np, nn, dout);
-  WS_CK(cudaMemcpyAsync(t->h_pin, dout, 32, cudaMemcpyDeviceToHost, s));
+  u64* hp = pin();
+  if (!hp) return WS_ERR_ALLOC;
+  WS_CK(cudaMemcpyAsync(hp, dout, 32, cudaMemcpyDeviceToHost, s));
   cudaFreeAsync(dout, s);
   WS_CK(cudaStreamSynchronize(s));
-  memcpy(out, t->h_pin, 32);
+  memcpy(out, hp, 32);
   return cuda_err(cudaGetLastError());
 }
 
@@ -1196,9 +1308,11 @@ int ws_duplicate_scan(ws_table* t, uint64_t* dup_keys, uint64_t* dup_counts, uin
     WS_CK(cudaMallocAsync(&tmp, tb + 16, s));
     cub::DeviceRadixSort::SortKeys(tmp, tb, k_in, k_out, (int64_t)cnt, 0, 64, s);
     k_dup_runs<<<grid_for(cnt), kThreads, 0, s>>>(k_out, cnt, dk, dc, cap_d, dn);
-    WS_CK(cudaMemcpyAsync(t->h_pin, dn, 8, cudaMemcpyDeviceToHost, s));
+    u64* hp = pin();
+    if (!hp) return WS_ERR_ALLOC;
+    WS_CK(cudaMemcpyAsync(hp, dn, 8, cudaMemcpyDeviceToHost, s));
     WS_CK(cudaStreamSynchronize(s));
-    ndup = t->h_pin[0];
+    ndup = hp[0];
     const u64 m = std::min<u64>(ndup, cap);
     if (m && dup_keys) WS_CK(cudaMemcpyAsync(dup_keys, dk, 8 * m, cudaMemcpyDefault, s));
     if (m && dup_counts) WS_CK(cudaMemcpyAsync(dup_counts, dc, 8 * m, cudaMemcpyDefault, s));
@@ -1225,6 +1339,21 @@ int ws_export_raw(ws_table* t, uint64_t* words, uint64_t nwords, uint16_t* tags,
     if (t->d.tags) WS_CK(cudaMemcpyAsync(tags, t->d.tags, 2 * t->d.cap, cudaMemcpyDefault, s));
     else WS_CK(cudaMemsetAsync(tags, 0, 0, s));
   }
+  WS_CK(cudaStreamSynchronize(s));
+  return WS_OK;
+}
+
+int ws_read_range(ws_table* t, uint64_t first_word, uint64_t nwords, uint64_t* words, uint64_t first_tag,
+                  uint64_t ntags, uint16_t* tags, void* stream) {
+  if (!t || (nwords && !words) || (ntags && !tags)) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  std::shared_lock<std::shared_mutex> lk(t->mu);
+  if (first_word > t->cell_words || nwords > t->cell_words - first_word) return WS_ERR_ARG;
+  const u64 ncap_tags = t->d.tags ? t->d.cap : 0;
+  if (first_tag > ncap_tags || ntags > ncap_tags - first_tag) return WS_ERR_ARG;
+  cudaStream_t s = S(stream);
+  if (nwords) WS_CK(cudaMemcpyAsync(words, t->d.cells + first_word, 8 * nwords, cudaMemcpyDefault, s));
+  if (ntags) WS_CK(cudaMemcpyAsync(tags, t->d.tags + first_tag, 2 * ntags, cudaMemcpyDefault, s));
   WS_CK(cudaStreamSynchronize(s));
   return WS_OK;
 }

@@ -120,7 +120,7 @@ __device__ __forceinline__ void ck_release(const Dev& d, const u64 (&srt)[W], in
 template <int W>
 __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* __restrict__ keys, u64 n,
                                                              u64* vout, u8* found, int gated) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const bool locked = !d.phased;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* _
 __global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* __restrict__ keys,
                                                               const u64* __restrict__ vals, u64 n, int merge,
                                                               u8* st_out, int gated) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const bool locked = true;  // mutations lock even in phased mode (Ctx::ck_lock_all)

@@ -88,7 +88,7 @@ __device__ __forceinline__ bool confirm(const Dev& d, u64 b, u32 M, u64 key, u64
 template <int Q, bool RO, int POL>
 __global__ void __launch_bounds__(256) k_query_p2md(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                     u8* found, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   u64 pol_tag = 0, pol_cell = 0;
   if (POL) {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_tag));
@@ -237,7 +237,7 @@ __device__ __forceinline__ int pair_confirm(const Dev& d, u64 b, u32 M, u64 key,
 template <bool RO, bool F64>
 __global__ void __launch_bounds__(256) k_query_p2md_pair(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                          u8* found, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   const Pair p;
   const u32 te0 = ld_u32_relaxed(d.state);
   const u64 stride = ((u64)gridDim.x * blockDim.x) >> 1;
@@ -300,7 +300,7 @@ __device__ __forceinline__ bool pair_lock_extra(const Dev& d, const Pair& p, u64
 static __global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __restrict__ keys,
                                                           const u64* __restrict__ vals, u64 n, int merge,
                                                           u8* status, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   const Pair p;
   const bool lead = p.half == 0;
   const u32 te0 = ld_u32_relaxed(d.state);
@@ -463,7 +463,7 @@ __device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16
 template <bool RO, bool F64, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                          u8* found, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   const u32 te0 = ld_u32_relaxed(d.state);
   const u64 stride = (u64)gridDim.x * blockDim.x;
   // the loop runs warp-uniformly: the bound is the warp's first index
@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
                                                             const u64* __restrict__ vals, u64 n, int merge,
                                                             u8* status, int conc_erase, int gated,
                                                             const u32* __restrict__ dmask = nullptr) {
-  if (gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3))) return;
+  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
   // bulk phase B (ws_bulk.cu): only the batch ops whose bit is set in dmask
   // (deferred by phase A) run; the rest already took effect.  Each warp
   // walks a contiguous range of bitmap words and packs up to 32 deferred ops

@@ -36,7 +36,7 @@ inline unsigned grid_for_table(u64 n, u64 nb, int threads = kThreads, int per_sm
 }
 
 __device__ __forceinline__ bool gate_closed(const Dev& d, int gated) {
-  return gated && (ld_u32_relaxed(d.state + 2) | ld_u32_relaxed(d.state + 3));
+  return gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1));
 }
 
 template <int DES, int BS, bool INSTR>
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kThreads) k_ops(Dev d, const u8* __restrict__ 
   Probe pr;
   if constexpr (INSTR) pp = &pr;
   // conc_erase 2: the launch's erase count (k_count_erases) decides
-  const bool conc = conc_erase == 2 ? ld_u32_relaxed(d.state + 4) != 0 : conc_erase != 0;
+  const bool conc = conc_erase == 2 ? ld_u32_relaxed(d.cs + 3) != 0 : conc_erase != 0;
   Ctx<DES, BS, false, INSTR> c{d, pp, conc, ld_u32_relaxed(d.state)};
   // rlist: a compacted list of the batch indices to run (*rcount of them),
   // so every lane of a warp has work (k_compact_retry)

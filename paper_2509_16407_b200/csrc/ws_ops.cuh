@@ -30,7 +30,11 @@ struct Dev {
   u64* cells;        // 2 words per slot, or the chaining node arena
   u16* tags;         // md designs
   u32* locks;        // 1 bit per bucket
-  u32* state;        // [0] tombstones_ever  [1] chain pool exhausted  [2] invalid keys
+  u32* state;        // [0] tombstones_ever (table-wide, persistent)
+  // per-call state (each API call gets its own 4 words, so concurrent calls on
+  // one table never see each other's verdicts): [0] invalid keys  [1] invalid
+  // op bytes  [2] chain pool exhausted  [3] erase count of a mixed batch
+  u32* cs;
   u64* chain_next;   // chaining bump allocator
   u64 chain_cap;     // physical node capacity of the arena
   u64* bfs_mem;      // cuckoo BFS workspaces
@@ -982,7 +986,7 @@ struct Ctx {
       }
       const u64 m = atomicAdd(d.chain_next, 1ull);
       if (m >= d.chain_cap) {
-        st_u32_relaxed(d.state + 1, 1u);  // host grows the pool and re-runs this op
+        st_u32_relaxed(d.cs + 2, 1u);  // host grows the pool and re-runs this op
         st = S_RETRY;
         break;
       }

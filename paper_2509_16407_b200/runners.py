@@ -10,6 +10,10 @@ schema CSV rows (instrument.Row).
 * ``run_aging``  prefill 0.85, then mixed batches: Zipf upsert-ADD on live
   keys + fresh inserts, erase of the oldest slice, queries on untouched live
   keys and on absent keys (reference runners.py:259-353; config 3)
+* ``run_aging_uniform``  the reference's own aging workload with its
+  instrumented probe phase (SPEC acceptance 8, Table 1 aging probes)
+* ``run_scaling``  probe means / throughput per table size (reference
+  runners.py:356-405; SPEC acceptance 13)
 * ``run_kmer``  canonical 31-mer counting with upsert-ADD (config 5 on one
   table / shard)
 """
@@ -263,6 +267,128 @@ def run_aging(design: str = "iceberg_md", capacity: int = 1 << 26, iterations: i
     return {"design": design, "capacity": cap, "slice": sl, "iterations": its, "ok": total_ok,
             "checksum_ok": got == want, "duplicates": t.duplicate_count(),
             "mean_mops": float(np.mean([i["mops"] for i in its])), "rows": rows}
+
+
+def _probe_means(t, ops, keys, vals, kinds):
+    """Serial instrumented pass (reference ProbeRecorder order); returns
+    {kind: mean distinct lines} for the contiguous op groups in `kinds`."""
+    st, vo, pr, _locks = t.probe_batch(ops, keys, vals, serial=True)
+    out, o = {}, 0
+    for kind, n in kinds:
+        if n:
+            out[kind] = float(pr[o:o + n].mean())
+        o += n
+    return st, vo, out
+
+
+def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_fraction: float = 0.01,
+                      seed: int = 42, probe_sample: int = 200, line_bytes: int = 128) -> dict:
+    """The reference's aging workload restated (bench/runners.py:259-353):
+    fill to 85%, then per iteration one concurrent mixed launch that inserts
+    a 1% slice of new keys (value k & 0xFFFF), erases the oldest 1%, queries
+    1% known-present and 1% known-absent keys -- interleaved by the
+    reference's (k * 0x9E3779B97F4A7C15) & 0xFFFFFFFF sort -- followed by the
+    instrumented probe phase on the first `probe_sample` keys of each slice
+    (upsert value 1, erase, present query, absent query; serial, as the
+    reference's single-threaded recorder).  Every result is checked."""
+    from .tables import OP_ERASE, OP_QUERY, OP_UPSERT, make_table
+    t = make_table(TableConfig(design=design, capacity_slots=capacity, seed=seed, line_bytes=line_bytes))
+    dev = t.device
+    cap = t.capacity_slots
+    fill_n = int(cap * 0.85)
+    slice_n = max(4, int(fill_n * slice_fraction))
+    stream = gen_uniform_keys(seed, fill_n + slice_n * iterations + 16)
+    neg_stream = gen_uniform_keys(derive_seed(seed, 0xADAE), slice_n * iterations + 16)
+    st = t.upsert_batch(_dev(stream[:fill_n], dev), _dev(stream[:fill_n] & U64(0xFFFF), dev))
+    if int((_np(st) == 2).sum()):
+        raise RuntimeError("aging prefill hit full")
+    probe_n = min(probe_sample, slice_n)
+    head, nxt = 0, fill_n
+    its, rows, ok_all = [], [], True
+    for it in range(iterations):
+        new_k = stream[nxt:nxt + slice_n]
+        old_k = stream[head:head + slice_n]          # FIFO = insertion order of the stream
+        pos_k = stream[head + slice_n:head + 2 * slice_n]
+        neg_k = neg_stream[it * slice_n:(it + 1) * slice_n]
+        kinds = np.concatenate([np.full(slice_n - probe_n, c, np.uint8) for c in (0, 1, 2, 3)])
+        keys = np.concatenate([new_k[probe_n:], old_k[probe_n:], pos_k[probe_n:], neg_k[probe_n:]])
+        order = np.argsort((keys * U64(0x9E3779B97F4A7C15)) & U64(0xFFFFFFFF), kind="stable")
+        kinds, keys = kinds[order], keys[order]
+        ops = np.where(kinds == 0, OP_UPSERT, np.where(kinds == 1, OP_ERASE, OP_QUERY)).astype(np.uint8)
+        vals = np.where(kinds == 0, keys & U64(0xFFFF), U64(0))
+        with _Timer() as tm:
+            s, _v = t.mixed_batch(_dev(ops, dev), _dev(keys, dev), _dev(vals, dev), check=False)
+        s = _np(s)
+        ok = bool((s[kinds == 0] == 0).all() and (s[kinds == 1] == 1).all() and
+                  (s[kinds == 2] == 1).all() and not s[kinds == 3].any())
+        p_ops = np.concatenate([np.full(probe_n, OP_UPSERT), np.full(probe_n, OP_ERASE),
+                                np.full(2 * probe_n, OP_QUERY)]).astype(np.uint8)
+        p_keys = np.concatenate([new_k[:probe_n], old_k[:probe_n], pos_k[:probe_n], neg_k[:probe_n]])
+        p_vals = np.concatenate([np.ones(probe_n, U64), np.zeros(3 * probe_n, U64)])
+        ps, _pv, means = _probe_means(t, p_ops, p_keys, p_vals,
+                                      [("insert", probe_n), ("erase", probe_n), ("query_pos", probe_n),
+                                       ("query_neg", probe_n)])
+        ok &= bool((ps[:probe_n] == 0).all() and (ps[probe_n:3 * probe_n] == 1).all() and
+                   not ps[3 * probe_n:].any())
+        ok_all &= ok
+        head += slice_n
+        nxt += slice_n
+        lf = round(fill_n / cap, 4)
+        rows.append(Row(design, "concurrent", cap, line_bytes, "throughput", "mixed", lf, 0, len(ops),
+                        tm.ms / 1e3, _mops(len(ops), tm.ms)))
+        for kind, m in means.items():
+            rows.append(Row(design, "concurrent", cap, line_bytes, "probe", kind, lf, 1, probe_n, 0.0, 0.0, m))
+        its.append({"iteration": it, "probe_means": means, "mops": _mops(len(ops), tm.ms), "ok": ok})
+    return {"design": design, "capacity": cap, "slice": slice_n, "iterations": its, "ok": ok_all,
+            "occupied": t.occupied_count(), "fill_n": fill_n, "rows": rows}
+
+
+def run_scaling(design: str, sizes=(1 << 17, 1 << 20, 1 << 23), seed: int = 42, probe_sample: int = 4096,
+                query_sample: int = 1 << 20, line_bytes: int = 128) -> dict:
+    """Insert to 90% and positive-query throughput plus probe means per table
+    size (reference bench/runners.py:356-405): the last stretch of the fill
+    is inserted instrumented, then instrumented positive / negative queries."""
+    from .tables import OP_QUERY, OP_UPSERT, make_table
+    per_size, rows = [], []
+    for size in sizes:
+        t = make_table(TableConfig(design=design, capacity_slots=size, seed=seed, line_bytes=line_bytes))
+        dev = t.device
+        cap = t.capacity_slots
+        fill_n = int(cap * 0.9)
+        probe_ins_n = min(probe_sample, max(1, fill_n // 5))
+        n = fill_n - probe_ins_n
+        keys = gen_uniform_keys(derive_seed(seed, size), fill_n)
+        dk = _dev(keys[:n], dev)
+        with _Timer() as ti:
+            st = t.upsert_batch(dk, _dev(keys[:n] & U64(0xFFFF), dev), check=False)
+        fulls = int((_np(st) == 2).sum())
+        stride = max(1, n // min(query_sample, n))
+        pos = keys[:n][::stride][:min(query_sample, n)]
+        with _Timer() as tq:
+            f, _v = t.query_batch(_dev(pos, dev), check=False)
+        miss = int((~_np(f).astype(bool)).sum())
+        ins_ops = np.full(probe_ins_n, OP_UPSERT, np.uint8)
+        pst, _pv, m_ins = _probe_means(t, ins_ops, keys[n:], np.ones(probe_ins_n, U64),
+                                       [("insert", probe_ins_n)])
+        fulls += int((pst == 2).sum())
+        ps = min(probe_sample, n)
+        pstride = max(1, fill_n // ps)
+        psample = keys[::pstride][:ps]
+        negs = gen_uniform_keys(derive_seed(seed, size, 3), probe_sample)
+        q_ops = np.full(len(psample) + len(negs), OP_QUERY, np.uint8)
+        _s, _v2, m_q = _probe_means(t, q_ops, np.concatenate([psample, negs]), None,
+                                    [("query_pos", len(psample)), ("query_neg", len(negs))])
+        means = {**m_ins, **m_q}
+        rows.append(Row(design, "concurrent", cap, line_bytes, "throughput", "insert", 0.9, 0, n, ti.ms / 1e3,
+                        _mops(n, ti.ms)))
+        rows.append(Row(design, "concurrent", cap, line_bytes, "throughput", "query_pos", 0.9, 0, len(pos),
+                        tq.ms / 1e3, _mops(len(pos), tq.ms)))
+        for kind, m in means.items():
+            rows.append(Row(design, "concurrent", cap, line_bytes, "probe", kind, 0.9, 1, 0, 0.0, 0.0, m))
+        per_size.append({"size": cap, "probe_means": means, "fulls": fulls, "missing": miss,
+                         "insert_mops": _mops(n, ti.ms), "query_mops": _mops(len(pos), tq.ms)})
+        del t
+    return {"design": design, "per_size": per_size, "rows": rows}
 
 
 def run_kmer(genome_len: int = 1 << 24, k: int = 31, capacity: int = 1 << 25, design: str = "p2_md",

@@ -209,10 +209,39 @@ class ShardedTable:
         out = self._a2a(res, send, recv)
         return self.router.unpermute(out, perm)
 
+    # ------------------------------------------------------------ validation
+    def _validate(self, keys, ops=None):
+        """Group-wide batch check before any routing or mutation: every rank
+        tests its own batch for sentinel keys (reference core.py:27-31,
+        103-117) and bad op bytes, the verdicts are all-reduced, and if any
+        rank's batch is invalid EVERY rank raises -- so no rank is left
+        waiting in an exchange and no shard has been changed (the whole
+        logical batch is rejected, as SPEC.md:89 asks of one table)."""
+        import torch
+        import torch.distributed as dist
+        from .core import InvalidKeyError
+        k = keys.view(torch.int64)
+        code = 2 if bool(((k == 0) | (k == -1) | (k == -2)).any()) else 0
+        if not code and ops is not None:
+            o = ops.to(torch.int32)
+            code = 1 if bool((((o & 15) > 2) | ((o >> 4) > 4)).any()) else 0
+        flag = torch.tensor([code], dtype=torch.int64,
+                            device="cpu" if self._host_staged() else self.local.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+        code = int(flag.item())
+        if code == 2:
+            raise InvalidKeyError("a batch on some rank contains a reserved sentinel key "
+                                  "(0, 2^64-1 or 2^64-2); the sharded batch was rejected on every rank")
+        if code == 1:
+            raise ValueError("a batch on some rank contains an invalid op byte (kind > 2 or merge > 4)")
+
     # ----------------------------------------------------------------- ops
     def upsert_batch(self, keys, values, merge=None, check=True):
         if self.world == 1:
             return self.local.upsert_batch(keys, values, merge=merge, check=check)
+        if check:
+            self._validate(keys)
+            check = False
         if self._xchg is not None:
             from .tables import OP_UPSERT, merge_id
             return self._p2p(keys, values, None, OP_UPSERT | (merge_id(merge) << 4), False, check)[0]
@@ -223,6 +252,9 @@ class ShardedTable:
     def query_batch(self, keys, check=True):
         if self.world == 1:
             return self.local.query_batch(keys, check=check)
+        if check:
+            self._validate(keys)
+            check = False
         if self._xchg is not None:
             from .tables import OP_QUERY
             st, vo = self._p2p(keys, None, None, OP_QUERY, True, check)
@@ -237,6 +269,9 @@ class ShardedTable:
     def erase_batch(self, keys, check=True):
         if self.world == 1:
             return self.local.erase_batch(keys, check=check)
+        if check:
+            self._validate(keys)
+            check = False
         if self._xchg is not None:
             from .tables import OP_ERASE
             return as_bool(self._p2p(keys, None, None, OP_ERASE, False, check)[0])
@@ -251,6 +286,9 @@ class ShardedTable:
             values = torch.zeros(keys.numel(), dtype=keys.dtype, device=keys.device)
         if self.world == 1:
             return self.local.mixed_batch(ops, keys, values, check=check)
+        if check:
+            self._validate(keys, ops)
+            check = False
         if self._xchg is not None:
             return self._p2p(keys, values, ops, 0, True, check)
         rk, rv, ro, perm, send, recv = self._route(keys, values, ops)

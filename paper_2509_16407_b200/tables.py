@@ -67,7 +67,10 @@ _MERGE_REF = (
     min,
 )
 _PROBE_PAIRS = ((5, 3), (3, 5), (0, 7), (7, 0), (U64, 2), (2, U64), (1 << 63, (1 << 63) + 5),
-                (123456789, 987654321), (U64, U64))
+                (123456789, 987654321), (U64, U64), (0, 0), (1, 1), (U64, 1), (1, U64),
+                (1 << 32, (1 << 32) - 1), ((1 << 32) - 1, 1 << 32)) + tuple(
+    (int(a), int(b)) for a, b in
+    np.random.default_rng(0x6D65726765).integers(0, 1 << 64, size=(48, 2), dtype=np.uint64))
 _merge_cache: dict = {}
 
 
@@ -102,6 +105,8 @@ def merge_id(merge) -> int:
         raise TypeError(f"merge callable {merge!r} failed on probe inputs: {exc}") from exc
     for mid, ref in enumerate(_MERGE_REF):
         if all(g == ref(a, b) for g, (a, b) in zip(got, _PROBE_PAIRS)):
+            if len(_merge_cache) > 4096:  # callables created per call must not pile up
+                _merge_cache.clear()
             _merge_cache[key] = (merge, mid)
             return mid
     raise TypeError(f"merge callable {merge!r} is not one of replace/keep/add/max/min; "
@@ -148,26 +153,28 @@ def _checked_out(t, n, dtype):
 
 class _Slots:
     """Read-only view of the device slot cells (quiescent test introspection,
-    mirrors reference sync.py WideSlotArray accessors)."""
+    mirrors reference sync.py WideSlotArray accessors).  Each accessor reads
+    only the cells it covers (ws_read_range), never the whole table."""
 
     def __init__(self, table):
         self._t = weakref.ref(table)
 
-    def _words(self):
-        return self._t()._raw()[0]
+    def _words(self, lo, hi):
+        """Cell words of slots [lo, hi) as uint64[2 * (hi - lo)]."""
+        return self._t()._read_words(2 * lo, 2 * (hi - lo))
 
     def __len__(self):
         return self._t().capacity_slots
 
     def key_at(self, i):
-        return int(self._words()[2 * i])
+        return int(self._words(i, i + 1)[0])
 
     def snapshot(self, i):
-        w = self._words()
-        return int(w[2 * i]), int(w[2 * i + 1])
+        w = self._words(i, i + 1)
+        return int(w[0]), int(w[1])
 
     def find_free(self, lo, hi):
-        keys = self._words()[2 * lo:2 * hi:2]
+        keys = self._words(lo, hi)[0::2]
         for j, k in enumerate(keys.tolist()):
             if k == 0:
                 return lo + j, True
@@ -176,15 +183,15 @@ class _Slots:
         return -1, False
 
     def used_count(self, lo, hi):
-        keys = self._words()[2 * lo:2 * hi:2]
+        keys = self._words(lo, hi)[0::2]
         return int(((keys != 0) & (keys != np.uint64(U64))).sum())
 
     def iter_occupied(self, lo, hi):
-        w = self._words()
-        for j in range(lo, hi):
+        w = self._words(lo, hi)
+        for j in range(hi - lo):
             k = int(w[2 * j])
             if k != 0 and k < U64 - 1:
-                yield j, k, int(w[2 * j + 1])
+                yield lo + j, k, int(w[2 * j + 1])
 
 
 class _Tags:
@@ -192,7 +199,7 @@ class _Tags:
         self._t = weakref.ref(table)
 
     def get(self, i):
-        return int(self._t()._raw()[1][i])
+        return int(self._t()._read_tags(i, 1)[0])
 
 
 class _Arena:
@@ -275,10 +282,6 @@ class HashTable:
         self._h = h
         self._raw_cache = None
         self._finalizer = weakref.finalize(self, lib.ws_destroy, h)
-        self._h1 = np.zeros(1, dtype=np.uint64)
-        self._v1 = np.zeros(1, dtype=np.uint64)
-        self._s1 = np.zeros(1, dtype=np.uint8)
-        self._o1 = np.zeros(1, dtype=np.uint8)
 
     # ------------------------------------------------------------ plumbing
     def _stream(self):
@@ -297,6 +300,8 @@ class HashTable:
         self._raw_cache = None
 
     def _raw(self):
+        """Whole cell array and tag array on the host (test introspection of
+        small tables only: 18 B per slot are copied)."""
         if self._raw_cache is None:
             nwords = self._info().node_bytes // 8 if self.design == "chaining" else 2 * self.capacity_slots
             words = np.empty(nwords, dtype=np.uint64)
@@ -305,6 +310,18 @@ class HashTable:
                                                 tags.ctypes.data, self._stream()))
             self._raw_cache = (words, tags)
         return self._raw_cache
+
+    def _read_words(self, first, n):
+        out = np.empty(n, dtype=np.uint64)
+        self._check(self._lib.ws_read_range(self._h, first, n, out.ctypes.data, 0, 0, None,
+                                            self._stream()))
+        return out
+
+    def _read_tags(self, first, n):
+        out = np.empty(n, dtype=np.uint16)
+        self._check(self._lib.ws_read_range(self._h, 0, 0, None, first, n, out.ctypes.data,
+                                            self._stream()))
+        return out
 
     def _info(self):
         info = _native.WsInfo()
@@ -340,38 +357,40 @@ class HashTable:
         check_key(key)
         check_value(value)
         m = merge_id(merge)
-        self._h1[0] = key
-        self._v1[0] = value
         if probe is not None:
             st, _v = self._probed(OP_UPSERT | (m << 4), key, value, probe)
             return _STATUS[st]
+        # per-call host scratch: scalar ops may be issued from many threads at
+        # once (reference tables/base.py:5-7); ctypes drops the GIL in the call
+        kv = np.array((key, value), dtype=np.uint64)
+        s1 = np.zeros(1, dtype=np.uint8)
         self._dirty()
-        self._check(self._lib.ws_upsert(self._h, self._h1.ctypes.data, self._v1.ctypes.data, 1, m,
-                                        self._s1.ctypes.data, self._stream(),
-                                        _native.WS_F_NO_CHECK))
-        return _STATUS[int(self._s1[0])]
+        self._check(self._lib.ws_upsert(self._h, kv.ctypes.data, kv.ctypes.data + 8, 1, m,
+                                        s1.ctypes.data, self._stream(), _native.WS_F_NO_CHECK))
+        return _STATUS[int(s1[0])]
 
     def query(self, key, probe=None):
         check_key(key)
-        self._h1[0] = key
         if probe is not None:
             found, v = self._probed(OP_QUERY, key, 0, probe)
             return v if found else None
-        self._check(self._lib.ws_query(self._h, self._h1.ctypes.data, 1, self._v1.ctypes.data,
-                                       self._s1.ctypes.data, self._stream(),
-                                       _native.WS_F_NO_CHECK))
-        return int(self._v1[0]) if self._s1[0] else None
+        kv = np.array((key, 0), dtype=np.uint64)
+        s1 = np.zeros(1, dtype=np.uint8)
+        self._check(self._lib.ws_query(self._h, kv.ctypes.data, 1, kv.ctypes.data + 8,
+                                       s1.ctypes.data, self._stream(), _native.WS_F_NO_CHECK))
+        return int(kv[1]) if s1[0] else None
 
     def erase(self, key, probe=None):
         check_key(key)
-        self._h1[0] = key
         if probe is not None:
             found, _v = self._probed(OP_ERASE, key, 0, probe)
             return bool(found)
+        k1 = np.array((key,), dtype=np.uint64)
+        s1 = np.zeros(1, dtype=np.uint8)
         self._dirty()
-        self._check(self._lib.ws_erase(self._h, self._h1.ctypes.data, 1, self._s1.ctypes.data,
+        self._check(self._lib.ws_erase(self._h, k1.ctypes.data, 1, s1.ctypes.data,
                                        self._stream(), _native.WS_F_NO_CHECK))
-        return bool(self._s1[0])
+        return bool(s1[0])
 
     def _probed(self, op, key, value, probe):
         """Run one op through the instrumented kernel and replay its probe
@@ -393,9 +412,9 @@ class HashTable:
 
     def slot_of(self, key):
         check_key(key)
-        self._h1[0] = key
+        k1 = np.array((key,), dtype=np.uint64)
         out = np.zeros(1, dtype=np.int64)
-        self._check(self._lib.ws_locate(self._h, self._h1.ctypes.data, 1, out.ctypes.data,
+        self._check(self._lib.ws_locate(self._h, k1.ctypes.data, 1, out.ctypes.data,
                                         self._stream()))
         return None if out[0] < 0 else int(out[0])
 
@@ -518,13 +537,19 @@ class HashTable:
         return zip(k.tolist(), v.tolist())
 
     def duplicate_scan(self) -> dict:
+        """{key: count} for every key stored more than once (reference
+        tables/base.py:151-156); every duplicate is returned, however many."""
         n = C.c_uint64()
         cap = 1 << 16
-        dk = np.empty(cap, dtype=np.uint64)
-        dc = np.empty(cap, dtype=np.uint64)
-        self._check(self._lib.ws_duplicate_scan(self._h, dk.ctypes.data, dc.ctypes.data, cap,
-                                                C.byref(n), self._stream()))
-        m = min(int(n.value), cap)
+        while True:
+            dk = np.empty(cap, dtype=np.uint64)
+            dc = np.empty(cap, dtype=np.uint64)
+            self._check(self._lib.ws_duplicate_scan(self._h, dk.ctypes.data, dc.ctypes.data, cap,
+                                                    C.byref(n), self._stream()))
+            if int(n.value) <= cap:
+                break
+            cap = int(n.value)  # quiescent table: the second scan returns the same set
+        m = int(n.value)
         return {int(a): int(b) for a, b in zip(dk[:m], dc[:m])}
 
     def duplicate_count(self) -> int:
@@ -636,7 +661,7 @@ class _BucketedTable(HashTable):
         bs = self.bucket_size
         lo = b * bs
         if self.md:
-            tags = self._raw()[1][lo:lo + bs]
+            tags = self._read_tags(lo, bs)
             zeros = min(int((tags == 0).sum()), self._d.zero_count_cap)
             return bs - zeros, zeros > 0
         used = self.slots.used_count(lo, lo + bs)

@@ -2,7 +2,8 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py          # small op streams + known answers
+    python tests/golden/make_golden.py --spec   # SPEC.md:659 10^5-op x 3-seed digests
 
 It imports the reference package (warpbench, pure Python) from
 /root/reference/pkg/src under the alias ``warpbench_ref`` and records:
@@ -185,7 +186,55 @@ def run_stream(design, stream, cap, seed, n_ops, universe_frac, extra=None, fill
     return res
 
 
+def spec_equivalence():
+    """SPEC.md:659 (acceptance 3): 10^5 seeded mixed ops x 3 seeds per design on
+    the reference tables through the scalar API (reference
+    tests/oracle.py:30-67 semantics), recorded as digests of the per-op
+    results, the final map and the final slot layout."""
+    sys.path.insert(0, OUT)
+    from spec_stream import (DESIGNS, MERGE_IDS, SPEC_CAPACITY, SPEC_OPS, SPEC_SEEDS,
+                             SPEC_TABLE_SEED, digest, items_digest, spec_stream)
+    fns = {0: MERGE_FN["add"], 1: MERGE_FN["keep"], 2: MERGE_FN["replace"], 3: None}
+    out = {"capacity": SPEC_CAPACITY, "table_seed": SPEC_TABLE_SEED, "n_ops": SPEC_OPS,
+           "seeds": list(SPEC_SEEDS), "merge_ids": list(MERGE_IDS), "streams": {}}
+    for d in DESIGNS:
+        cfg = rcore.TableConfig(design=d, capacity_slots=_cap_for(d, SPEC_CAPACITY), seed=SPEC_TABLE_SEED)
+        for seed in SPEC_SEEDS:
+            t = make_table(cfg)
+            ops, keys, vals, midx = spec_stream(t.capacity_slots, SPEC_OPS, seed)
+            status = np.zeros(SPEC_OPS, dtype=np.uint8)
+            qvals = np.zeros(SPEC_OPS, dtype=np.uint64)
+            for i in range(SPEC_OPS):
+                k, kind = int(keys[i]), int(ops[i]) & 15
+                if kind == 0:
+                    status[i] = STATUS[t.upsert(k, int(vals[i]), fns[midx[i]])]
+                elif kind == 1:
+                    status[i] = int(t.erase(k))
+                else:
+                    got = t.query(k)
+                    if got is not None:
+                        status[i], qvals[i] = 1, got
+            items = list(t.items())
+            rec = {"status": digest(status), "qvals": digest(qvals),
+                   "items": items_digest([a for a, _ in items], [b for _, b in items]),
+                   "n_items": len(items), "fulls": int((status[ops & 15 == 0] == 2).sum())}
+            if d == "chaining":
+                a = t.arena
+                w = np.array(a.words[: a.wpn * a.next_node], dtype=np.uint64).reshape(-1, a.wpn)
+                rec["layout"] = digest(w[:, list(range(0, a.wpn - 2, 2)) + [a.wpn - 2]])  # keys + link
+            else:
+                rec["layout"] = digest(np.array([t.slots.key_at(i) for i in range(t.capacity_slots)],
+                                                dtype=np.uint64))
+            out["streams"][f"{d}/{seed}"] = rec
+            print("spec", d, seed, rec["n_items"], rec["fulls"], flush=True)
+    with open(os.path.join(OUT, "spec_equivalence.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 def main():
+    if "--spec" in sys.argv:
+        spec_equivalence()
+        return
     hash_kat()
     for d in ALL:
         cap = 7 * 128 if d == "chaining" else 1024

@@ -24,6 +24,27 @@ def test_safe_p2md_large_no_delay():
     assert rep["duplicate_buckets"] == 0, rep
 
 
+@pytest.mark.parametrize("design", SAFE)
+def test_spec_scale_hundred_trials_co_scheduled(design):
+    """SPEC.md:657 acceptance: >= 100 trials x 10^4 primary buckets (the
+    reference CLI default, cli.py:321-322), the three actors of each bucket
+    in adjacent warps of one CTA (actor_layout), light delays: 0 duplicates."""
+    from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
+    rep = run_adversarial(design, buckets=10_000, trials=100, seed=7, profile=DelayProfile(0.04, 5_000))
+    assert rep["trials"] == 100 and rep["replays"] == 1_000_000
+    assert rep["duplicate_buckets"] == 0, rep
+
+
+def test_unsafe_reference_races_at_spec_scale():
+    """The positive control at the same scale finds duplicates (co-scheduled
+    actors, no delays needed to expose the lock-elided race)."""
+    from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
+    rep = run_adversarial("unsafe_reference", buckets=10_000, trials=100, seed=7,
+                          profile=DelayProfile(0.04, 5_000))
+    assert rep["duplicate_buckets"] >= 1, rep
+    assert sum(1 for d in rep["per_trial"] if d) >= 10, rep["per_trial"]
+
+
 def test_unsafe_reference_races():
     from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
     rep = run_adversarial("unsafe_reference", buckets=20_000, trials=3, seed=5,

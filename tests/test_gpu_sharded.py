@@ -105,3 +105,53 @@ def test_sharded_two_ranks_one_gpu(exchange):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def _kmer_worker(rank, world, port, outq, exchange):
+    """BASELINE config 5 in miniature: canonical 31-mer counting with
+    upsert-ADD through ShardedTable (reads split over the ranks, every k-mer
+    routed to its owner), then every distinct k-mer queried from every rank;
+    counts must equal numpy's global multiplicities exactly."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2509_16407_b200 import TableConfig
+        from paper_2509_16407_b200.sharded import ShardedTable
+        from paper_2509_16407_b200.workload import kmer_keys
+        st = ShardedTable(TableConfig(design="p2_md", capacity_slots=1 << 21, seed=42), exchange=exchange,
+                          chunk_ops=1 << 17)
+        km = kmer_keys(1 << 20, 31, seed=9, repeats=4)        # ~2^20 k-mers, ~2^18 distinct
+        rng = np.random.default_rng(5)
+        km = km[rng.permutation(len(km))]
+        mine = km[rank::world]                                # this rank's reads
+        for part in np.array_split(mine, 3):
+            s = _np(st.upsert_batch(_cu(part), _cu(np.ones(len(part), U64)), merge="add"))
+            assert ((s == 0) | (s == 1)).all()
+        u, c = np.unique(km, return_counts=True)
+        f, v = st.query_batch(_cu(u))
+        assert _np(f).all()
+        assert (_np(v) == c.astype(U64)).all()
+        assert st.occupied_count() == len(u)
+        assert st.duplicate_count() == 0
+        dist.barrier()
+        dist.destroy_process_group()
+        outq.put((rank, "ok"))
+    except Exception:  # noqa: BLE001
+        import traceback
+        outq.put((rank, traceback.format_exc()))
+        raise
+
+
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_config5_kmer_counting_two_ranks(exchange):
+    ctx = mp.get_context("spawn")
+    outq = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_kmer_worker, args=(r, 2, port, outq, exchange)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(outq.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res

@@ -16,7 +16,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN
+from conftest import GOLDEN, cfg_for
 from oracle import OracleTable, build_oracle
 from paper_2509_16407_b200.core import TableConfig
 
@@ -114,3 +114,42 @@ def test_oracle_sequential_matches_survey_kats():
     assert fam.bucket(0, 1, 1 << 23) == 5800346
     assert fam.bucket(1, 1, 1 << 23) == 1511528
     assert core.fingerprint(fam, 0x123456789ABCDEF0) == 0xBC36
+
+
+def _spec():
+    import sys
+    sys.path.insert(0, GOLDEN)
+    import spec_stream
+    return spec_stream, json.load(open(os.path.join(GOLDEN, "spec_equivalence.json")))
+
+
+def spec_layout(design, words_or_slot_keys, next_node=None):
+    """Layout digest input: slot keys, or chaining node keys + link words."""
+    if design == "chaining":
+        w = np.asarray(words_or_slot_keys, dtype=np.uint64)[: 16 * next_node].reshape(-1, 16)
+        return w[:, list(range(0, 14, 2)) + [14]]
+    return np.asarray(words_or_slot_keys, dtype=np.uint64)
+
+
+@pytest.mark.parametrize("design", ["double", "double_md", "p2", "p2_md", "iceberg", "iceberg_md",
+                                    "cuckoo", "chaining"])
+def test_oracle_spec_scale_equivalence(design):
+    """SPEC.md:659 acceptance 3 at its stated scale: 10^5 seeded mixed ops x 3
+    seeds per design (reference tests/oracle.py:30-67 stream), every per-op
+    result, the final map and the final layout equal to the reference's."""
+    ss, spec = _spec()
+    cfg = cfg_for(design, spec["capacity"], seed=spec["table_seed"])
+    for seed in spec["seeds"]:
+        ref = spec["streams"][f"{design}/{seed}"]
+        t = OracleTable(cfg)
+        ops, keys, vals, _ = ss.spec_stream(t.capacity_slots, spec["n_ops"], seed)
+        st, qv = t.mixed_batch(ops, keys, vals)
+        assert ss.digest(st) == ref["status"], (design, seed)
+        assert ss.digest(qv) == ref["qvals"], (design, seed)
+        k, v = t.items_arrays()
+        assert len(k) == ref["n_items"] and ss.items_digest(k, v) == ref["items"]
+        if design == "chaining":
+            lay = spec_layout(design, t.words(), t.next_node)
+        else:
+            lay = spec_layout(design, t.slot_keys())
+        assert ss.digest(lay) == ref["layout"], (design, seed)

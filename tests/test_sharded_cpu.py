@@ -155,6 +155,23 @@ def _worker(rank, world, port, outq):
         f, _ = st.query_batch(t64(mine))
         assert not f.numpy()[::2].any() and f.numpy()[1::2].all()
         assert st.duplicate_count() == 0
+        # a sentinel key in ONE rank's batch rejects the logical
+        # batch on EVERY rank before any routing or mutation (no hang)
+        from paper_2509_16407_b200 import InvalidKeyError
+        before = st.checksum()
+        fresh = gen_uniform_keys(555 + rank, 1000)
+        if rank == 1:
+            fresh[321] = U64(0xFFFFFFFFFFFFFFFF)  # TOMBSTONE sentinel
+        with pytest.raises(InvalidKeyError):
+            st.upsert_batch(t64(fresh), t64(fresh))
+        with pytest.raises(InvalidKeyError):
+            st.erase_batch(t64(fresh))
+        bad_ops = torch.zeros(1000, dtype=torch.uint8)
+        if rank == 0:
+            bad_ops[5] = 7  # kind 7 does not exist
+        with pytest.raises(ValueError):
+            st.mixed_batch(bad_ops, t64(gen_uniform_keys(556 + rank, 1000)))
+        assert st.checksum() == before
         dist.barrier()
         dist.destroy_process_group()
         outq.put((rank, "ok"))
