@@ -1,12 +1,19 @@
 """Benchmark: P2-MD (power-of-two-choice + fingerprint metadata) hash table,
 insert to 0.9 load then 50/50 hit/miss lock-free queries (BASELINE.json
-config 2: 2^28 slots on one B200).
+config 2's workload at the north-star size: 2^30 slots on one B200;
+--log2-slots 28 gives config 2's stated size).
 
 One step = clear the table, insert n = int(0.9 * slots) uniform keys
 (values k & 0xFFFF, reference runners.py:104) in one batch, then query n keys
-(half inserted, half absent, shuffled) in one batch.  Inputs are generated
-once and stay resident in HBM; the table (4.5 GiB) and the key batches
-(1.9 GiB each) dwarf the 126 MB L2, so no flush is needed between steps.
+(half inserted, half absent, shuffled) in one batch, both with the batch-wide
+sentinel check on (the product default).  Inputs are generated once and stay
+resident in HBM; the table (18 GiB at 2^30) and the key batches (7.7 GB each)
+dwarf the 126 MB L2, so no flush is needed between steps.
+
+After the timed run, rank 0 re-runs one step of the same workload under
+`ncu` (DRAM sectors and duration of the insert and query kernels only) to
+report MEASURED bytes per op beside the algorithmic ones (roofline.traffic,
+roofline.measured); WS_BENCH_NCU=0 skips it.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
@@ -57,12 +64,75 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--log2-slots", type=int, default=28)
+    ap.add_argument("--log2-slots", type=int, default=30)
     ap.add_argument("--load", type=float, default=0.9)
     ap.add_argument("--design", default="p2_md")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
+
+
+# ------------------------------------------------------ measured traffic
+
+INSERT_KERNEL = "k_upsert_p2md_rounds"
+QUERY_KERNEL = "k_query_p2md_coop"
+
+
+def measured_traffic(args, timeout_s=420):
+    """One step of this workload under ncu: DRAM sectors read + written and
+    duration of the insert and query launches of the SECOND step (the first
+    is warm-up).  Returns {kernel: {"dram_bytes", "read_bytes", "write_bytes",
+    "ncu_ms"}} or {"error": ...}."""
+    import csv
+    import shutil
+    import subprocess
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"error": "ncu not found"}
+    log = tempfile.NamedTemporaryFile(suffix=".csv", delete=False).name
+    cmd = [ncu, "--metrics", "dram__sectors_read.sum,dram__sectors_write.sum,gpu__time_duration.sum",
+           "--kernel-name", f"regex:{INSERT_KERNEL}|{QUERY_KERNEL}", "--launch-skip", "2", "--launch-count", "2",
+           "--clock-control", "none", "--csv", "--log-file", log,
+           sys.executable, os.path.abspath(__file__), "--traffic-probe", "--log2-slots", str(args.log2_slots),
+           "--load", str(args.load), "--design", args.design]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s,
+                           env={**os.environ, "WS_BENCH_NCU": "0"})
+    except subprocess.TimeoutExpired:
+        return {"error": f"ncu run exceeded {timeout_s} s"}
+    out = {}
+    try:
+        rows = [r_ for r_ in csv.reader(open(log)) if len(r_) > 10]
+    except OSError:
+        rows = []
+    if rows:
+        hdr = rows[0]
+        ki, mi, vi = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+        ui = hdr.index("Metric Unit")
+        for row in rows[1:]:
+            name = INSERT_KERNEL if INSERT_KERNEL in row[ki] else QUERY_KERNEL if QUERY_KERNEL in row[ki] else None
+            if not name:
+                continue
+            v = float(row[vi].replace(",", ""))
+            d = out.setdefault(name, {"kernel_signature": row[ki][:160]})
+            if row[mi] == "dram__sectors_read.sum":
+                d["read_bytes"] = int(v * 32)
+            elif row[mi] == "dram__sectors_write.sum":
+                d["write_bytes"] = int(v * 32)
+            elif row[mi] == "gpu__time_duration.sum":
+                d["ncu_ms"] = v / 1e6 if row[ui] == "ns" else v / 1e3 if row[ui] == "us" else v
+    for d in out.values():
+        if "read_bytes" in d and "write_bytes" in d:
+            d["dram_bytes"] = d["read_bytes"] + d["write_bytes"]
+    try:
+        os.unlink(log)
+    except OSError:
+        pass
+    if INSERT_KERNEL not in out or QUERY_KERNEL not in out:
+        return {"error": f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-300:]}"}
+    return out
 
 
 # ------------------------------------------------------------------ clocks
@@ -200,6 +270,11 @@ def run_ours(args, rank, world):
     from paper_2509_16407_b200.workload import derive_seed, gen_uniform_keys
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+    # the ncu traffic capture runs first, in a child process, while this one
+    # holds no device memory yet (N = 1 only: ncu must not see several ranks)
+    meas = {"error": "skipped (N>1, WS_BENCH_NCU=0 or traffic probe)"}
+    if world == 1 and not args.traffic_probe and os.environ.get("WS_BENCH_NCU", "1") != "0":
+        meas = measured_traffic(args)
     torch.cuda.set_device(dev)
     host_coll = dist.is_initialized() and dist.get_backend() == "gloo"
 
@@ -240,14 +315,19 @@ def run_ours(args, rank, world):
         table.clear()
         if i is not None:
             ev[i][0].record(stream)
-        st = table.upsert_batch(keys, vals, check=False)
+        st = table.upsert_batch(keys, vals)
         if i is not None:
             ev[i][1].record(stream)
-        found, qv = table.query_batch(q, check=False)
+        found, qv = table.query_batch(q)
         if i is not None:
             ev[i][2].record(stream)
         return st, found, qv
 
+    if args.traffic_probe:  # under ncu (measured_traffic): two steps, nothing else
+        step()
+        step()
+        torch.cuda.synchronize()
+        return
     # correctness gate on the first warm-up step (not timed)
     st, found, qv = step()
     torch.cuda.synchronize()
@@ -327,18 +407,29 @@ def run_ours(args, rank, world):
     qry_bytes = (QUERY_TABLE_B + QUERY_IO_B) * n
     ins_gbs = ins_bytes / (ms_ins / 1000) / 1e9
     qry_gbs = qry_bytes / (ms_qry / 1000) / 1e9
-    traffic = qtraffic = None
-    ceiling = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            pj = json.load(open(prof))
-            if pj.get("log2_slots") == args.log2_slots and pj.get("design") == args.design:
-                traffic = pj.get("insert_dram_bytes_per_launch")
-                qtraffic = pj.get("query_dram_bytes_per_launch")
-            ceiling = pj.get("random_request_ceiling_g_per_s")
-        except Exception:  # noqa: BLE001
-            traffic = None
+    # live DRAM traffic of this build at this size (one step under ncu, above)
+    mi, mq = meas.get(INSERT_KERNEL, {}), meas.get(QUERY_KERNEL, {})
+    traffic, qtraffic = mi.get("dram_bytes"), mq.get("dram_bytes")
+
+    def measured(d, ms_k):
+        if not d.get("dram_bytes"):
+            return None
+        bpo = d["dram_bytes"] / n
+        return {"dram_bytes_per_launch": d["dram_bytes"], "read_bytes": d["read_bytes"],
+                "write_bytes": d["write_bytes"], "bytes_per_op": round(bpo, 2),
+                "sectors_per_op": round(bpo / 32, 3), "ncu_ms_cold": round(d.get("ncu_ms", 0.0), 3),
+                "achieved_gbs": round(d["dram_bytes"] / (ms_k / 1000) / 1e9, 1),
+                "frac": round(d["dram_bytes"] / (ms_k / 1000) / 1e9 / peak, 4)}
+    ceiling, ceiling_src = None, None
+    for name in ("random_access_ceiling.json", "ncu_traffic.json"):
+        prof = os.path.join(ROOT, "profiles", name)
+        if ceiling is None and os.path.exists(prof):
+            try:
+                pj = json.load(open(prof))
+                ceiling = pj.get("random_request_ceiling_g_per_s")
+                ceiling_src = f"scripts/gather_bench.cu (profiles/{name})"
+            except Exception:  # noqa: BLE001
+                ceiling = None
     cpu = None
     if not args.no_cpu_baseline:
         threads = 1
@@ -371,6 +462,12 @@ def run_ours(args, rank, world):
             "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(ins_gbs / peak, 4),
             "traffic": traffic,
             "algorithmic_bytes_per_op": INSERT_TABLE_B + INSERT_IO_B,
+            # north-star form: ops/s x MEASURED DRAM bytes per op (ncu, this build, this size)
+            # against the measured copy peak, for both kernels
+            "measured": {"insert": measured(mi, ms_ins), "query": measured(mq, ms_qry),
+                         "source": "ncu dram__sectors_read/write.sum of step 2 of this workload "
+                                   "(bench.py --traffic-probe), divided by the CUDA-event kernel time above",
+                         "error": meas.get("error")},
             "query_kernel": {"kernel": "k_query_p2md_coop", "achieved": round(qry_gbs, 1),
                              "frac": round(qry_gbs / peak, 4),
                              "algorithmic_bytes_per_op": QUERY_TABLE_B + QUERY_IO_B,
@@ -378,7 +475,7 @@ def run_ours(args, rank, world):
             "random_access": {
                 "unit": "G random DRAM line accesses/s (reads + write-backs)",
                 "ceiling": ceiling,
-                "ceiling_source": "scripts/gather_bench.cu (profiles/ncu_traffic.json)",
+                "ceiling_source": ceiling_src,
                 "insert_requests_per_op": INSERT_REQ, "query_requests_per_op": QUERY_REQ,
                 "insert_achieved": round(n * INSERT_REQ / ms_ins / 1e6, 2),
                 "query_achieved": round(n * QUERY_REQ / ms_qry / 1e6, 2),
@@ -393,7 +490,8 @@ def run_ours(args, rank, world):
         "e2e": {"value": round(e2e_val, 1), "unit": UNIT,
                 "h2d_bytes_per_step": int(n * 24), "d2h_bytes_per_step": int(n * 10),
                 "path": "ws_upsert/ws_query C ABI with pinned host buffers"},
-        "gpu_launches": (2 if world == 1 else (2 * (2 + 2 * world + 3)
+        # per step: sentinel check + upsert kernel, sentinel check + query kernel
+        "gpu_launches": (4 if world == 1 else (2 * (2 + 2 * world + 3)
                                                  if table.exchange == "p2p" else 11)) * args.steps,
         "clocks": clk.report(),
     }

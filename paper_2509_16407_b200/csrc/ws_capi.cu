@@ -56,11 +56,31 @@ __global__ void k_count_erases(const u8* __restrict__ ops, u64 n, u32* cs) {
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(cs + 3, c);
 }
 
-__global__ void k_validate(const u64* __restrict__ keys, const u8* __restrict__ ops, u64 n, u32* cs) {
+// Batch-wide sentinel / op-byte check, run before any mutation.  A pure
+// streaming pass (8 B per key): 16-byte streaming loads, 4 per thread in
+// flight, so the pass runs near the copy bandwidth (2^30 keys: ~1.2 ms).
+__global__ void __launch_bounds__(256) k_validate(const u64* __restrict__ keys, const u8* __restrict__ ops, u64 n,
+                                                  u32* cs) {
   u32 bad_k = 0, bad_o = 0;
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-    bad_k += is_sentinel(__ldg(keys + i));
-    if (ops) {
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x, nt = (u64)gridDim.x * blockDim.x;
+  const bool vec = ((uintptr_t)keys & 15) == 0;
+  const u64 npair = vec ? n / 2 : 0;
+  const ulonglong2* kp = (const ulonglong2*)keys;
+  u64 j = tid;
+  for (; j + 3 * nt < npair; j += 4 * nt) {
+    ulonglong2 v[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) v[r] = __ldcs(kp + j + r * nt);
+#pragma unroll
+    for (int r = 0; r < 4; r++) bad_k += is_sentinel(v[r].x) + is_sentinel(v[r].y);
+  }
+  for (; j < npair; j += nt) {
+    const ulonglong2 v = __ldcs(kp + j);
+    bad_k += is_sentinel(v.x) + is_sentinel(v.y);
+  }
+  for (u64 i = 2 * npair + tid; i < n; i += nt) bad_k += is_sentinel(__ldg(keys + i));
+  if (ops) {
+    for (u64 i = tid; i < n; i += nt) {
       const u8 o = __ldg(ops + i);
       bad_o += ((o & 15) > OP_QUERY) | ((o >> 4) > M_MIN);
     }
@@ -258,7 +278,7 @@ Mod make_mod(u64 d) {
 int validate(const u64* keys, const u8* ops, u64 n, cudaStream_t s, bool sync, u32 flags, const CallCtx& cx) {
   if (flags & WS_F_NO_CHECK) return WS_OK;
   WS_CK(cudaMemsetAsync(cx.cs, 0, 2 * sizeof(u32), s));
-  if (n) k_validate<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(keys, ops, n, cx.cs);
+  if (n) k_validate<<<grid_for(n / 2 + 1, kThreads, 8), kThreads, 0, s>>>(keys, ops, n, cx.cs);
   WS_CK(cudaGetLastError());
   if (!sync) return WS_OK;
   u64* hp = pin();
@@ -809,7 +829,7 @@ int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
     if (ho) WS_CK(cudaMemcpyAsync((void*)(dops + off), ops + off, m, cudaMemcpyHostToDevice, sg->s_in));
     WS_CK(cudaEventRecord(sg->ev_in, sg->s_in));
     WS_CK(cudaStreamWaitEvent(s, sg->ev_in, 0));
-    if (check) k_validate<<<grid_for(m, kThreads, 4), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
+    if (check) k_validate<<<grid_for(m / 2 + 1, kThreads, 8), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
                                                                          cx.cs);
     return cuda_err(cudaGetLastError());
   };
@@ -858,7 +878,7 @@ int run_staged(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
       for (u64 c = 0; c < nch; c++) {
         const u64 off = c * chunk, m = std::min(chunk, n - off);
         WS_CK(cudaStreamWaitEvent(s, sg->ev_chunk[c], 0));
-        k_validate<<<grid_for(m, kThreads, 4), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
+        k_validate<<<grid_for(m / 2 + 1, kThreads, 8), kThreads, 0, s>>>(dk + off, dops ? dops + off : nullptr, m,
                                                                  cx.cs);
       }
       WS_CK(cudaGetLastError());

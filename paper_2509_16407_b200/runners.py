@@ -269,10 +269,12 @@ def run_aging(design: str = "iceberg_md", capacity: int = 1 << 26, iterations: i
             "mean_mops": float(np.mean([i["mops"] for i in its])), "rows": rows}
 
 
-def _probe_means(t, ops, keys, vals, kinds):
-    """Serial instrumented pass (reference ProbeRecorder order); returns
-    {kind: mean distinct lines} for the contiguous op groups in `kinds`."""
-    st, vo, pr, _locks = t.probe_batch(ops, keys, vals, serial=True)
+def _probe_means(t, ops, keys, vals, kinds, serial=False):
+    """Instrumented pass; returns {kind: mean distinct lines} for the
+    contiguous op groups in `kinds`.  The ops of one pass touch distinct keys,
+    so each op's probe count is that of its own path whether the pass runs
+    serially (the reference's single recorder) or one thread per op."""
+    st, vo, pr, _locks = t.probe_batch(ops, keys, vals, serial=serial)
     out, o = {}, 0
     for kind, n in kinds:
         if n:
@@ -344,10 +346,13 @@ def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_f
 
 
 def run_scaling(design: str, sizes=(1 << 17, 1 << 20, 1 << 23), seed: int = 42, probe_sample: int = 4096,
-                query_sample: int = 1 << 20, line_bytes: int = 128) -> dict:
+                query_sample: int = 1 << 20, line_bytes: int = 128, probe_window: float = 0.0) -> dict:
     """Insert to 90% and positive-query throughput plus probe means per table
     size (reference bench/runners.py:356-405): the last stretch of the fill
-    is inserted instrumented, then instrumented positive / negative queries."""
+    is inserted instrumented, then instrumented positive / negative queries.
+    probe_window > 0 sizes that stretch as a load fraction (the same load
+    window at every size) instead of the reference's min(probe_sample,
+    fill / 5) keys."""
     from .tables import OP_QUERY, OP_UPSERT, make_table
     per_size, rows = [], []
     for size in sizes:
@@ -355,7 +360,8 @@ def run_scaling(design: str, sizes=(1 << 17, 1 << 20, 1 << 23), seed: int = 42, 
         dev = t.device
         cap = t.capacity_slots
         fill_n = int(cap * 0.9)
-        probe_ins_n = min(probe_sample, max(1, fill_n // 5))
+        probe_ins_n = (max(1, int(cap * probe_window)) if probe_window > 0
+                       else min(probe_sample, max(1, fill_n // 5)))
         n = fill_n - probe_ins_n
         keys = gen_uniform_keys(derive_seed(seed, size), fill_n)
         dk = _dev(keys[:n], dev)

@@ -2,7 +2,10 @@
 //
 // Each thread performs R independent random reads of W bytes (W = 16, 32, 64,
 // 128) at W-aligned positions of a large buffer (>> L2), addresses from a
-// splitmix64 hash (no index array), and XOR-folds the data.  Variants:
+// splitmix64 hash masked to the (power-of-two) buffer -- no index array and
+// no 64-bit division, so the kernel is not issue-bound -- and XOR-folds the
+// data.  Mode 'm' sweeps memory-level parallelism (CTAs/SM x loads in flight)
+// and the cooperative one-instruction block reads of gather_coop.  Variants:
 //   flavor 0: weak loads (ld.global, L1 allocate)
 //   flavor 1: ld.global.nc.L1::no_allocate
 //   flavor 2: ld.relaxed.gpu (coherent, what mutating kernels use)
@@ -43,7 +46,7 @@ __global__ void __launch_bounds__(256) gather(const char* buf, u64 nunits, u64 s
   for (int it = 0; it < iters; it++) {
     u64 idx[R];
 #pragma unroll
-    for (int r = 0; r < R; r++) idx[r] = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) % nunits;
+    for (int r = 0; r < R; r++) idx[r] = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) & (nunits - 1);
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const char* p = buf + idx[r] * W;
@@ -57,6 +60,46 @@ __global__ void __launch_bounds__(256) gather(const char* buf, u64 nunits, u64 s
   if (acc == 0x123456789ull) out[0] = acc;
 }
 
+// Cooperative form: a group of G consecutive lanes reads one random
+// (32*G)-byte block with ONE load instruction (lane l of the group takes the
+// l-th 32-byte sector), the access pattern of the pair-cooperative tag fetch.
+// Counts blocks/s, i.e. random DRAM line accesses of 32*G bytes.
+template <int G, int R>
+__global__ void __launch_bounds__(256) gather_coop(const char* buf, u64 nblocks, u64 seed, u64* out, int iters) {
+  u64 acc = 0;
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  const u64 grp = tid / G;
+  const int sub = (int)(tid % G);
+  for (int it = 0; it < iters; it++) {
+    u64 idx[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) idx[r] = mix64(seed ^ (grp * R + r) ^ ((u64)it << 40)) & (nblocks - 1);
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      u64 a, b, c, d;
+      ld32<3>(buf + idx[r] * (32 * G) + 32 * sub, a, b, c, d);
+      acc ^= a ^ b ^ c ^ d;
+    }
+  }
+  if (acc == 0x123456789ull) out[0] = acc;
+}
+
+template <int G, int R>
+void run_coop(const char* buf, u64 bytes, u64* out, int blocks, int iters, const char* name) {
+  const u64 nb = bytes / (32 * G);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  gather_coop<G, R><<<blocks, 256>>>(buf, nb, 1, out, 1);
+  cudaEventRecord(a);
+  gather_coop<G, R><<<blocks, 256>>>(buf, nb, 7, out, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double acc = (double)blocks * 256 / G * R * iters;
+  printf("%-28s W=%4d R=%d  %8.2f G blocks/s  %8.1f GB/s useful\n", name, 32 * G, R, acc / ms / 1e6,
+         acc * 32 * G / ms / 1e6);
+}
+
 // random stores of W bytes (2, 16 or 32) at W-aligned positions
 template <int W, int R>
 __global__ void __launch_bounds__(256) scatter(char* buf, u64 nunits, u64 seed, int iters) {
@@ -64,7 +107,7 @@ __global__ void __launch_bounds__(256) scatter(char* buf, u64 nunits, u64 seed, 
   for (int it = 0; it < iters; it++) {
 #pragma unroll
     for (int r = 0; r < R; r++) {
-      const u64 idx = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) % nunits;
+      const u64 idx = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) & (nunits - 1);
       char* p = buf + idx * W;
       if (W == 2) asm volatile("st.global.u16 [%0], %1;" :: "l"(p), "h"((unsigned short)tid) : "memory");
       else if (W == 16) asm volatile("st.global.v2.u64 [%0], {%1, %2};" :: "l"(p), "l"(tid), "l"(idx) : "memory");
@@ -84,7 +127,7 @@ __global__ void __launch_bounds__(256) readwrite(char* buf, u64 nunits, u64 seed
     char* p[R];
 #pragma unroll
     for (int r = 0; r < R; r++) {
-      p[r] = buf + (mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) % nunits) * 64;
+      p[r] = buf + (mix64(seed ^ (tid * R + r) ^ ((u64)it << 40)) & (nunits - 1)) * 64;
       asm volatile("ld.relaxed.gpu.global.L2::64B.v4.u64 {%0,%1,%2,%3}, [%4];"
                    : "=l"(a[r][0]), "=l"(a[r][1]), "=l"(a[r][2]), "=l"(a[r][3]) : "l"(p[r]) : "memory");
     }
@@ -144,13 +187,34 @@ void run(const char* buf, u64 bytes, u64* out, int blocks, int iters, const char
 }
 
 int main(int argc, char** argv) {
-  const u64 mb = argc > 1 ? strtoull(argv[1], 0, 10) : 4096;
+  const u64 mb = argc > 1 ? strtoull(argv[1], 0, 10) : 4096;  // a power of two (index masks)
   const u64 bytes = mb << 20;
   printf("buffer %llu MiB\n", mb);
   char* buf; u64* out;
   cudaMalloc(&buf, bytes); cudaMalloc(&out, 64);
   cudaMemset(buf, 1, bytes);
   const int blocks = 148 * 8, iters = 16;
+  if (argc > 2 && argv[2][0] == 'm') {  // memory-level-parallelism sweep: is ~45 G/s a plateau?
+    for (int bps : {1, 2, 4, 8}) {
+      printf("-- %d CTAs/SM x 256 threads\n", bps);
+      const int bl = 148 * bps;
+      run<32, 3, 1>(buf, bytes, out, bl, iters, "nc L2::64B 32B");
+      run<32, 3, 2>(buf, bytes, out, bl, iters, "nc L2::64B 32B");
+      run<32, 3, 4>(buf, bytes, out, bl, iters, "nc L2::64B 32B");
+      run<32, 3, 8>(buf, bytes, out, bl, iters, "nc L2::64B 32B");
+      run<32, 3, 16>(buf, bytes, out, bl, iters, "nc L2::64B 32B");
+      run<32, 3, 32>(buf, bytes, out, bl, iters, "nc L2::64B 32B");
+      run<32, 1, 16>(buf, bytes, out, bl, iters, "nc (128B fill) 32B");
+      run<64, 3, 16>(buf, bytes, out, bl, iters, "nc L2::64B 64B");
+      run<128, 1, 8>(buf, bytes, out, bl, iters, "nc 128B");
+      run_coop<2, 8>(buf, bytes, out, bl, iters, "coop 2 lanes (1 instr)");
+      run_coop<2, 16>(buf, bytes, out, bl, iters, "coop 2 lanes (1 instr)");
+      run_coop<4, 8>(buf, bytes, out, bl, iters, "coop 4 lanes (1 instr)");
+      run_coop<4, 16>(buf, bytes, out, bl, iters, "coop 4 lanes (1 instr)");
+    }
+    cudaDeviceSynchronize();
+    return 0;
+  }
   if (argc > 2 && argv[2][0] == 'r') {  // read-then-write-same-sector
     run_rw<0, 4>(buf, bytes, out, blocks, iters, "read 32B only");
     run_rw<1, 4>(buf, bytes, out, blocks, iters, "read 32B + 2B store same sector");
