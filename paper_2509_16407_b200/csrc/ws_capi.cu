@@ -1055,6 +1055,7 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.tune_l2pol = 2;
   d.tune_upsert = 4;
   d.tune_occ = 0;
+  d.tune_pf = 0;  // measured slower at 2^28 and 2^30 (profiles/prefetch_r02.log)
   d.ck_resume = 0;
   t->tune_bulk = 0;  // measured slower than the per-op kernel at 2^28
   t->tune_bulk_gb = -1;
@@ -1411,8 +1412,12 @@ int ws_tune(ws_table* t, int knob, int value) {
       if (value < -1 || value > 8) return WS_ERR_ARG;
       t->tune_bulk_gb = value;
       return WS_OK;
-    case WS_TUNE_UPSERT:
+    case WS_TUNE_PREFETCH:
       if (value < 0 || value > 4) return WS_ERR_ARG;
+      t->d.tune_pf = value;
+      return WS_OK;
+    case WS_TUNE_UPSERT:
+      if (value < 0 || value > 5) return WS_ERR_ARG;
       t->d.tune_upsert = value;
       return WS_OK;
     default: return WS_ERR_ARG;

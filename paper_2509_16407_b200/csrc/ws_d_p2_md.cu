@@ -43,7 +43,18 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
 #define WS_UR(F, MB, PH) k_upsert_p2md_rounds<F, MB, PH><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, \
                                                    a.n, a.uop >> 4, a.status, a.conc_erase, a.gated)
     const bool f64 = a.d.tune_upsert >= 3;
-    if (a.d.tune_upsert == 4 && !a.d.phased) {
+    if (a.d.tune_upsert == 5 && !a.d.phased) {
+      k_upsert_p2md_rounds<true, 1, false, true, false, true><<<(unsigned)g, 256, 0, a.s>>>(
+          a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status, a.conc_erase, a.gated);
+    } else if (a.d.tune_upsert == 4 && !a.d.phased && a.d.tune_occ == 4) {
+      k_upsert_p2md_rounds<true, 4, false, true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n,
+                                                                                a.uop >> 4, a.status,
+                                                                                a.conc_erase, a.gated);
+    } else if (a.d.tune_upsert == 4 && !a.d.phased && a.d.tune_occ == 5) {
+      k_upsert_p2md_rounds<true, 5, false, true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n,
+                                                                                a.uop >> 4, a.status,
+                                                                                a.conc_erase, a.gated);
+    } else if (a.d.tune_upsert == 4 && !a.d.phased) {
       k_upsert_p2md_rounds<true, 1, false, true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n,
                                                                                 a.uop >> 4, a.status,
                                                                                 a.conc_erase, a.gated);

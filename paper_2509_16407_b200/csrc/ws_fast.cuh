@@ -179,6 +179,23 @@ struct Pair {
   __device__ __forceinline__ u32 from_lead(u32 v) const { return __shfl_sync(mask, v, (threadIdx.x & 31) & 30); }
 };
 
+// Software pipelining across grid-stride iterations: a lane hashes the key it
+// will handle `dist` iterations later and prefetches that op's primary tag
+// block (64 B, exactly the block: cp.async.bulk.prefetch) into L2, so when the
+// op comes up its tag load is an L2 hit instead of a DRAM round trip.  Pure
+// cache hint -- the op still reads the block itself (under its lock for
+// mutations), so correctness never depends on the prefetched copy.
+// (a bulk prefetch per lane goes through the TMA unit and measured 28-38%
+// slower: the LSU prefetch below is what a per-lane random block wants)
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" :: "l"(p) : "memory");
+}
+__device__ __forceinline__ void prefetch_tag_block(const Dev& d, const u64* __restrict__ keys, u64 i, u64 n) {
+  if (i >= n) return;
+  const u16* blk = d.tags + d.nbm(mix64(__ldg(keys + i) ^ d.seeds[0]) >> 16) * 32;
+  prefetch_l2(blk);
+}
+
 // 64-byte L2 fetch: the default promotes every random miss to a 128-byte
 // line fill (4 sectors, measured); a 64-byte tag block or a 16-byte cell only
 // needs 2 (scripts/gather_bench.cu: 3.92 -> 1.98 DRAM sectors per access).
@@ -426,8 +443,13 @@ __device__ __forceinline__ void half_masks(const u32 (&w)[8], u16 tag, u32& m, u
   }
 }
 
+// fence_after_issue (warp-uniform): one fence.acq_rel between issuing the
+// tag loads and consuming them -- the insert kernel's deferred lock release
+// (k_upsert_p2md_rounds, DEFER) overlaps the previous round's store
+// acknowledgements with this round's tag-load latency.
 template <bool RO, bool F64>
-__device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16 tag, u32& M, u32& Z) {
+__device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16 tag, u32& M, u32& Z,
+                                           bool fence_after_issue = false) {
   const int half = threadIdx.x & 1;
   const u64 pb = __shfl_xor_sync(0xFFFFFFFFu, b, 1);
   const u32 pt = __shfl_xor_sync(0xFFFFFFFFu, (u32)tag, 1);
@@ -449,6 +471,7 @@ __device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16
     if (F64) { if (RO) ld_tags32_ro64(pB, wB); else ld_tags32_64(pB, wB); }
     else { if (RO) ld_tags32_ro(pB, wB); else ld_tags32(pB, wB); }
   }
+  if (fence_after_issue) fence_acq_rel();
   u32 mA, zA, mB, zB;
   half_masks(wA, tA, mA, zA);
   half_masks(wB, tB, mB, zB);
@@ -467,8 +490,12 @@ __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64*
   const u32 te0 = ld_u32_relaxed(d.state);
   const u64 stride = (u64)gridDim.x * blockDim.x;
   // the loop runs warp-uniformly: the bound is the warp's first index
-  for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n; base += stride) {
+  const u64 first = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull;
+  const int pf = d.tune_pf;
+  for (int k = 1; k < pf; k++) prefetch_tag_block(d, keys, first + k * stride + (threadIdx.x & 31), n);
+  for (u64 base = first; base < n; base += stride) {
     const u64 i = base + (threadIdx.x & 31);
+    if (pf) prefetch_tag_block(d, keys, i + pf * stride, n);
     const bool act = i < n;
     const u64 key = act ? __ldg(keys + i) : 0;
     const u64 h0 = mix64(key ^ d.seeds[0]);
@@ -505,7 +532,7 @@ __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64*
 // under the bucket lock; storing (0,0) there too makes the 32-byte sector
 // fully valid in L2, so its eviction needs no ECC read-modify-write of the
 // untouched half (measured ~1 DRAM sector per insert without it).
-template <bool F64, int MINB, bool PHASED, bool FILL = false, bool MASK = false>
+template <bool F64, int MINB, bool PHASED, bool FILL = false, bool MASK = false, bool DEFER = false>
 __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, int merge,
                                                             u8* status, int conc_erase, int gated,
@@ -528,8 +555,17 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
     cw = c0 * per;
     whi = cw + per < mwords ? cw + per : mwords;
   }
+  const int pf = MASK ? 0 : d.tune_pf;
+  // DEFER: locks of ops finished in a warp's last round of a chunk are
+  // released after the NEXT chunk's first tag loads are issued, behind the
+  // one fence that also orders those loads -- the fence's wait for this
+  // round's store acknowledgements overlaps the next op's DRAM latency
+  // instead of stalling the warp on its own (ncu: membar was 31% of stalls)
+  u64 rel0 = ~0ull, rel1 = ~0ull;
+  for (int k = 1; k < pf; k++) prefetch_tag_block(d, keys, (c0 + k * nwarps) * 32 + lane, n);
   for (u64 c = c0; MASK ? cw < whi : c * 32 < n; c += nwarps) {
     u64 i = c * 32 + lane;
+    if (pf) prefetch_tag_block(d, keys, (c + pf * nwarps) * 32 + lane, n);
     bool pending = i < n;
     if constexpr (MASK) {
       const u64 wi = cw + lane;
@@ -592,7 +628,13 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
       bool drop0 = false;
       // phase 2: primary tag blocks, one request per op
       u32 M0, Z0;
-      coop_masks<false, F64>(d, hold0, b0, tag, M0, Z0);
+      const bool dfence = DEFER && __any_sync(0xFFFFFFFFu, rel0 != ~0ull || rel1 != ~0ull);
+      coop_masks<false, F64>(d, hold0, b0, tag, M0, Z0, dfence);
+      if (DEFER && dfence) {  // the fence inside coop_masks ordered the deferred ops' stores
+        if (rel1 != ~0ull) red_and_relaxed(d.locks + (rel1 >> 5), ~(1u << (rel1 & 31)));
+        if (rel0 != ~0ull) red_and_relaxed(d.locks + (rel0 >> 5), ~(1u << (rel0 & 31)));
+        rel0 = rel1 = ~0ull;
+      }
       bool hold1 = false, need1 = false, decided = false, te_last = true;
       u64 old;
       int used0 = 0;
@@ -673,15 +715,23 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
       // phase 4: one MEMBAR for the warp, then relaxed releases of the
       // finished lanes' locks (pending lanes keep what they hold, see above)
       if (!PHASED) {
-        __syncwarp();
-        fence_acq_rel();
-        if (held1 && !pending) {
-          red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
-          held1 = false;
-        }
-        if (held0 && (!pending || drop0)) {
-          red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
-          held0 = false;
+        // DEFER: when the chunk is done (no lane retries -- a retrying lane's
+        // backoff would stretch the hold), hand the releases to the next
+        // chunk's fence instead of fencing here
+        if (DEFER && !__any_sync(0xFFFFFFFFu, pending)) {
+          if (held1) { rel1 = b1; held1 = false; }
+          if (held0) { rel0 = b0; held0 = false; }
+        } else {
+          __syncwarp();
+          fence_acq_rel();
+          if (held1 && !pending) {
+            red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
+            held1 = false;
+          }
+          if (held0 && (!pending || drop0)) {
+            red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+            held0 = false;
+          }
         }
       }
       if (pending) {
@@ -690,6 +740,11 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
       }
     }
     if (status && (MASK ? mine : i < n)) status[i] = st;
+  }
+  if (DEFER && !PHASED && __any_sync(0xFFFFFFFFu, rel0 != ~0ull || rel1 != ~0ull)) {
+    fence_acq_rel();
+    if (rel1 != ~0ull) red_and_relaxed(d.locks + (rel1 >> 5), ~(1u << (rel1 & 31)));
+    if (rel0 != ~0ull) red_and_relaxed(d.locks + (rel0 >> 5), ~(1u << (rel0 & 31)));
   }
 }
 

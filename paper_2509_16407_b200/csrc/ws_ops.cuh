@@ -49,6 +49,7 @@ struct Dev {
   int tune_l2pol;  // 1: tag loads evict_last, cell loads evict_first
   int tune_upsert; // P2-MD upsert kernel: 0 generic one-thread-per-op, 1 lane pair, 2/3 rounds
   int tune_occ;    // minimum resident CTAs per SM requested from ptxas (register cap)
+  int tune_pf;     // tuned P2-MD kernels: L2 prefetch distance in grid-stride iterations (0 = off)
   // cuckoo: this launch continues ops whose first attempt (the locked scan
   // that found every bucket full) already ran in k_upsert_cuckoo_rounds, so
   // ck_upsert starts at the eviction search (launch-local, never stored)

@@ -20,6 +20,6 @@ for d in ('double', 'p2_md', 'double_md', 'p2', 'iceberg_md'):
             n = int(t.capacity_slots * 0.85)
             k = gen_uniform_keys(42, n)
             kd = torch.from_numpy(k.view(np.int64)).cuda().view(torch.uint64)
-            st = t.upsert_batch(kd, kd & 0xFFFF)
+            st = t.upsert_batch(kd, kd)
             fulls.append(int((st == 2).sum()))
         print(d, cap, fulls, flush=True)
