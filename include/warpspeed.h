@@ -174,12 +174,9 @@ WS_API int ws_info(ws_table *t, ws_info_t *info);
 #define WS_TUNE_DELAY_NS 5
 #define WS_TUNE_DELAY_P16 6
 #define WS_TUNE_DELAY_SEED 7
-#define WS_TUNE_BULK 8      /* P2-MD bucket-partitioned bulk upsert: 0 off, 1 auto (large uniform upsert
-                               batches, >= 4 ops per bucket), 2 whenever eligible */
 #define WS_TUNE_PREFETCH 10  /* tuned P2-MD upsert / query: prefetch the primary tag block of the op
                                this lane handles `value` grid-stride iterations ahead into L2
-                               (0 = off; default 1) */
-#define WS_TUNE_BULK_GROUP 9 /* bulk path: log2 buckets per owner group (0..8), -1 = from batch density */
+                               (0 = off, the default: measured slower, profiles/prefetch_r02.log) */
 WS_API int ws_tune(ws_table *t, int knob, int value);
 
 /* hash-sharded multi-GPU routing (device pointers): split a batch into

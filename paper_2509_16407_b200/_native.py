@@ -40,8 +40,6 @@ WS_TUNE_OCCUPANCY = 4
 WS_TUNE_DELAY_NS = 5
 WS_TUNE_DELAY_P16 = 6
 WS_TUNE_DELAY_SEED = 7
-WS_TUNE_BULK = 8
-WS_TUNE_BULK_GROUP = 9
 WS_TUNE_PREFETCH = 10
 
 

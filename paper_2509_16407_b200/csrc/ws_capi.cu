@@ -21,7 +21,6 @@
 #include <cub/cub.cuh>
 
 #include "warpspeed.h"
-#include "ws_bulk.cuh"
 #include "ws_kernels.cuh"
 
 using namespace ws;
@@ -178,9 +177,6 @@ struct ws_table {
   // streams are private to the call / calling thread (CallCtx, pin(),
   // staging()), so nothing else on the host side is shared.
   std::shared_mutex mu;
-  std::atomic<bool> maybe_tomb;  // an erase may have run since creation / clear (host hint for the bulk path)
-  int tune_bulk;    // WS_TUNE_BULK: 0 off, 1 auto, 2 always when eligible
-  int tune_bulk_gb; // WS_TUNE_BULK_GROUP: buckets per group log2 (-1 = from the batch density)
 };
 
 namespace {
@@ -243,11 +239,13 @@ Staging* staging(int device) {
 struct CallCtx {
   u32* cs;
   std::shared_lock<std::shared_mutex>* lk;
+  const u64* dn = nullptr;  // device-resident batch size (ws_internal_run from the exchange), n = upper bound
 };
 
 inline Dev dev_of(const ws_table* t, const CallCtx& cx) {
   Dev d = t->d;
   d.cs = cx.cs;
+  d.dn = cx.dn;
   return d;
 }
 
@@ -317,27 +315,6 @@ int chain_grow(ws_table* t, cudaStream_t s) {
   WS_CK(cudaMemcpyAsync(t->d.chain_next, hp, 8, cudaMemcpyHostToDevice, s));
   WS_CK(cudaStreamSynchronize(s));
   return WS_OK;
-}
-
-// Run one batch whose buffers are all device-resident.
-// Bucket-partitioned bulk upsert (ws_bulk.cu): P2-MD with default buckets,
-// uniform upsert batches much larger than the bucket count, tables whose
-// launches are not concurrent across streams (phase A relies on ownership, not
-// locks) and that never tombstoned (phase A is the shortcut regime).
-bool bulk_eligible(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u32 flags, cudaStream_t s) {
-  if (t->cfg.design != D_P2_MD || !t->def_bs || (uop & 15) != OP_UPSERT || t->tune_bulk == 0) return false;
-  if ((flags & WS_F_SERIAL) || t->cfg.multi_stream || t->cfg.phased || t->d.lock_elided) return false;
-  if (n >= (1ull << 32) || !bulk_aligned(keys, vals)) return false;
-  if (t->tune_bulk == 1 && (n < (1ull << 20) || n < 4 * t->d.nb)) return false;
-  if (t->maybe_tomb) {  // an erase ran: ask the device whether it ever tombstoned
-    u64* hp = pin();
-    if (!hp || cudaMemcpyAsync(hp, t->d.state, sizeof(u32), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-      return false;
-    if (*(const u32*)hp) return false;
-    t->maybe_tomb = false;
-  }
-  return true;
 }
 
 __global__ void k_comb_iota(u64 n, u32* idx);
@@ -452,7 +429,7 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
 int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                      bool query_only, const CallCtx& cx) {
-  if (ops && !query_only && n >= (1u << 16) && n < (1ull << 32) && !t->d.delay_ns &&
+  if (ops && !query_only && n >= (1u << 16) && n < (1ull << 32) && !t->d.delay_ns && !cx.dn &&
       !(flags & (WS_F_SERIAL | WS_F_INTERLEAVED | kF_NO_KIND_SORT)))
     return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, cx);
   const bool sync = (flags & WS_F_SYNC_CHECK) != 0;
@@ -460,13 +437,6 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
   if (rc) return rc;
   if (!n) return WS_OK;
   const int gated = (flags & kF_VALIDATED) ? 1 : (flags & WS_F_NO_CHECK) ? 0 : 1;
-  if (has_erase) t->maybe_tomb = true;
-  if (!query_only && !ops && bulk_eligible(t, uop, keys, vals, n, flags, s)) {
-    BulkPlan plan = bulk_plan(n, t->d.nb, t->tune_bulk_gb);
-    plan.skip_b = t->tune_bulk == 3;
-    plan.cap = std::max(0, t->d.shortcut - 4);
-    return cuda_err(bulk_upsert_p2md(dev_of(t, cx), keys, vals, n, uop >> 4, status, gated, s, plan));
-  }
   int conc = (has_erase || t->cfg.multi_stream) ? 1 : 0;
   if (ops && !t->cfg.multi_stream && !(flags & WS_F_SERIAL)) {
     // let the device decide: conc_erase = 2 reads the erase count at launch
@@ -612,7 +582,7 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
                u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                bool query_only, const CallCtx& cx) {
   if (!(flags & WS_F_COMBINE) || query_only || !has_upsert || n < 2 || n >= (1ull << 32) ||
-      (flags & WS_F_SERIAL))
+      (flags & WS_F_SERIAL) || cx.dn)
     return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s, flags & ~WS_F_COMBINE, has_erase,
                             has_upsert, query_only, cx);
   int rc = validate(keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
@@ -979,11 +949,16 @@ int compact_items(ws_table* t, cudaStream_t s, ulonglong2** out, u64* count) {
 }  // namespace
 
 // internal (not exported): device-pointer batch execution for ws_shard.cu
+// n_dev != nullptr: the batch size lives on the device (an exchange inbox
+// count); n is its upper bound.  Such batches run unvalidated, uncombined and
+// without the per-kind split (all of which need n on the host).
 int ws_internal_run(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
-                    u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, bool query_only) {
+                    u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, bool query_only,
+                    const u64* n_dev) {
   if (cudaSetDevice(t->device) != cudaSuccess) return WS_ERR_CUDA;
+  if (n_dev) flags = (flags & ~(WS_F_SYNC_CHECK | WS_F_COMBINE)) | WS_F_NO_CHECK;
   std::shared_lock<std::shared_mutex> lk(t->mu);
-  CallCtx cx{nullptr, &lk};
+  CallCtx cx{nullptr, &lk, n_dev};
   WS_CK(cudaMallocAsync((void**)&cx.cs, 4 * sizeof(u32), s));
   int rc = cuda_err(cudaMemsetAsync(cx.cs, 0, 4 * sizeof(u32), s));
   if (!rc) rc = run_device(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, query_only, cx);
@@ -1057,9 +1032,6 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.tune_occ = 0;
   d.tune_pf = 0;  // measured slower at 2^28 and 2^30 (profiles/prefetch_r02.log)
   d.ck_resume = 0;
-  t->tune_bulk = 0;  // measured slower than the per-op kernel at 2^28
-  t->tune_bulk_gb = -1;
-  t->maybe_tomb = false;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };
   if (c.design == D_CHAINING) {
@@ -1146,7 +1118,6 @@ int ws_clear(ws_table* t, void* stream) {
   if (d.tags) WS_CK(cudaMemsetAsync(d.tags, 0, d.cap * 2, s));
   WS_CK(cudaMemsetAsync(d.locks, 0, t->lock_words * 4, s));
   WS_CK(cudaMemsetAsync(d.state, 0, N_STATE * 4, s));
-  t->maybe_tomb = false;
   if (t->cfg.design == D_CHAINING) {
     u64* hp = pin();
     if (!hp) return WS_ERR_ALLOC;
@@ -1403,14 +1374,6 @@ int ws_tune(ws_table* t, int knob, int value) {
       return WS_OK;
     case WS_TUNE_DELAY_SEED:
       t->d.delay_seed = mix64((u64)(unsigned)value);
-      return WS_OK;
-    case WS_TUNE_BULK:
-      if (value < 0 || value > 3) return WS_ERR_ARG;
-      t->tune_bulk = value;
-      return WS_OK;
-    case WS_TUNE_BULK_GROUP:
-      if (value < -1 || value > 8) return WS_ERR_ARG;
-      t->tune_bulk_gb = value;
       return WS_OK;
     case WS_TUNE_PREFETCH:
       if (value < 0 || value > 4) return WS_ERR_ARG;

@@ -120,7 +120,7 @@ __device__ __forceinline__ void ck_release(const Dev& d, const u64 (&srt)[W], in
 template <int W>
 __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* __restrict__ keys, u64 n,
                                                              u64* vout, u8* found, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const bool locked = !d.phased;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* _
 __global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* __restrict__ keys,
                                                               const u64* __restrict__ vals, u64 n, int merge,
                                                               u8* st_out, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const bool locked = true;  // mutations lock even in phased mode (Ctx::ck_lock_all)
@@ -240,7 +240,9 @@ __global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* 
 
 // Warp-aggregated compaction of the S_RETRY ops into an index list (order
 // within a warp kept, across warps arbitrary: the ops are concurrent anyway).
-__global__ void __launch_bounds__(256) k_compact_retry(const u8* __restrict__ st, u64 n, u32* list, u32* count) {
+__global__ void __launch_bounds__(256) k_compact_retry(const u8* __restrict__ st, u64 n, u32* list, u32* count,
+                                                       const u64* dn) {
+  if (dn && *dn < n) n = *dn;  // device-resident batch size (multi-GPU exchange)
   const int lane = threadIdx.x & 31;
   for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n;
        base += (u64)gridDim.x * blockDim.x) {
@@ -275,7 +277,7 @@ static void cuckoo_ops(const OpsArgs& a, bool def) {
       if (a.n < 0xFFFFFFFFull && cudaMallocAsync((void**)&rl, 4 * (a.n + 1), a.s) == cudaSuccess) {
         cudaMemsetAsync(rl + a.n, 0, 4, a.s);
         k_compact_retry<<<(unsigned)std::max<u64>(std::min<u64>((a.n + 255) / 256, (u64)kSMs * 8), 1), 256, 0,
-                          a.s>>>(st, a.n, rl, rl + a.n);
+                          a.s>>>(st, a.n, rl, rl + a.n, a.d.dn);
         lo.rlist = rl;
         lo.rcount = rl + a.n;
       }

@@ -43,7 +43,7 @@ __device__ __forceinline__ void scan8(const u64 (&w)[16], u64 lo, u64 key, i64& 
 template <bool RO>
 __global__ void __launch_bounds__(256) k_query_double_lines(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                             u8* found, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const u64 len = (u64)d.probe_cap < d.nb ? (u64)d.probe_cap : d.nb;
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     const u64 key = __ldg(keys + i);
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) k_query_double_lines(Dev d, const u64* __
 __global__ void __launch_bounds__(256) k_upsert_double_rounds(Dev d, const u64* __restrict__ keys,
                                                               const u64* __restrict__ vals, u64 n, int merge,
                                                               u8* status, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const u64 len = (u64)d.probe_cap < d.nb ? (u64)d.probe_cap : d.nb;

@@ -13,7 +13,7 @@ namespace ws {
 template <bool RO>
 __global__ void __launch_bounds__(256) k_query_ice_lines(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                          u8* found, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     const u64 key = __ldg(keys + i);
     const u64 b0 = d.frontm(mix64(key ^ d.seeds[0]) >> 16);
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) k_query_ice_lines(Dev d, const u64* __res
 __global__ void __launch_bounds__(256) k_upsert_ice_rounds(Dev d, const u64* __restrict__ keys,
                                                            const u64* __restrict__ vals, u64 n, int merge,
                                                            u8* status, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const u32 te0 = ld_u32_relaxed(d.state);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;

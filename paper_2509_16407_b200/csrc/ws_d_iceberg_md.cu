@@ -26,7 +26,7 @@ template <bool FILL>
 __global__ void __launch_bounds__(256) k_upsert_icemd_rounds(Dev d, const u64* __restrict__ keys,
                                                              const u64* __restrict__ vals, u64 n, int merge,
                                                              u8* status, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const u32 te0 = ld_u32_relaxed(d.state);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;

@@ -1,6 +1,5 @@
 // Kernel instantiations for the p2_md design (the headline path): the generic
 // kernels of ws_kernels.cuh plus the tuned multi-lookup query of ws_fast.cuh.
-#include "ws_bulk.cuh"
 #include "ws_fast.cuh"
 #include "ws_kernels.cuh"
 
@@ -44,7 +43,7 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
                                                    a.n, a.uop >> 4, a.status, a.conc_erase, a.gated)
     const bool f64 = a.d.tune_upsert >= 3;
     if (a.d.tune_upsert == 5 && !a.d.phased) {
-      k_upsert_p2md_rounds<true, 1, false, true, false, true><<<(unsigned)g, 256, 0, a.s>>>(
+      k_upsert_p2md_rounds<true, 1, false, true, true><<<(unsigned)g, 256, 0, a.s>>>(
           a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status, a.conc_erase, a.gated);
     } else if (a.d.tune_upsert == 4 && !a.d.phased && a.d.tune_occ == 4) {
       k_upsert_p2md_rounds<true, 4, false, true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n,
@@ -117,12 +116,6 @@ static void p2_md_preload(bool def) {
   preload_fn(k_query_p2md_coop<true, true, 1>);
   preload_fn(k_upsert_p2md_rounds<true, 1, false, true>);
   preload_fn(k_upsert_p2md_rounds<true, 1, true>);
-  bulk_preload();
-}
-void bulk_phase_b(const Dev& d, const u64* keys, const u64* vals, u64 n, int merge, u8* status, int gated,
-                  const u32* dmask, unsigned grid, cudaStream_t s) {
-  k_upsert_p2md_rounds<true, 1, false, true, true><<<grid, 256, 0, s>>>(d, keys, vals, n, merge, status, 0, gated,
-                                                                        dmask);
 }
 
 Launchers launchers_p2_md() { return Launchers{p2_md_ops, p2_md_query, p2_md_locate, p2_md_preload}; }

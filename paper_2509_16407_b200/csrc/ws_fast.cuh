@@ -88,7 +88,7 @@ __device__ __forceinline__ bool confirm(const Dev& d, u64 b, u32 M, u64 key, u64
 template <int Q, bool RO, int POL>
 __global__ void __launch_bounds__(256) k_query_p2md(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                     u8* found, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   u64 pol_tag = 0, pol_cell = 0;
   if (POL) {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_tag));
@@ -254,7 +254,7 @@ __device__ __forceinline__ int pair_confirm(const Dev& d, u64 b, u32 M, u64 key,
 template <bool RO, bool F64>
 __global__ void __launch_bounds__(256) k_query_p2md_pair(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                          u8* found, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const Pair p;
   const u32 te0 = ld_u32_relaxed(d.state);
   const u64 stride = ((u64)gridDim.x * blockDim.x) >> 1;
@@ -317,7 +317,7 @@ __device__ __forceinline__ bool pair_lock_extra(const Dev& d, const Pair& p, u64
 static __global__ void __launch_bounds__(256) k_upsert_p2md_pair(Dev d, const u64* __restrict__ keys,
                                                           const u64* __restrict__ vals, u64 n, int merge,
                                                           u8* status, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const Pair p;
   const bool lead = p.half == 0;
   const u32 te0 = ld_u32_relaxed(d.state);
@@ -486,7 +486,7 @@ __device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16
 template <bool RO, bool F64, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
                                                          u8* found, int conc_erase, int gated) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
+  WS_PROLOGUE(d, gated, n);
   const u32 te0 = ld_u32_relaxed(d.state);
   const u64 stride = (u64)gridDim.x * blockDim.x;
   // the loop runs warp-uniformly: the bound is the warp's first index
@@ -532,30 +532,16 @@ __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64*
 // under the bucket lock; storing (0,0) there too makes the 32-byte sector
 // fully valid in L2, so its eviction needs no ECC read-modify-write of the
 // untouched half (measured ~1 DRAM sector per insert without it).
-template <bool F64, int MINB, bool PHASED, bool FILL = false, bool MASK = false, bool DEFER = false>
+template <bool F64, int MINB, bool PHASED, bool FILL = false, bool DEFER = false>
 __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, int merge,
-                                                            u8* status, int conc_erase, int gated,
-                                                            const u32* __restrict__ dmask = nullptr) {
-  if (gated && (ld_u32_relaxed(d.cs) | ld_u32_relaxed(d.cs + 1))) return;
-  // bulk phase B (ws_bulk.cu): only the batch ops whose bit is set in dmask
-  // (deferred by phase A) run; the rest already took effect.  Each warp
-  // walks a contiguous range of bitmap words and packs up to 32 deferred ops
-  // (whole words) into its lanes per pass, so lanes stay busy at ~30% density;
-  // the visiting order is batch order within each warp's range, as for the
-  // full per-op launch.
+                                                            u8* status, int conc_erase, int gated) {
+  WS_PROLOGUE(d, gated, n);
   const u32 te0 = ld_u32_relaxed(d.state);
   const int lane = threadIdx.x & 31;
   const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
   const u64 c0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
-  __shared__ u64 mpos[MASK ? 8 : 1][32];
-  u64 cw = 0, whi = 0;
-  if constexpr (MASK) {
-    const u64 mwords = (n + 31) / 32, per = (mwords + nwarps - 1) / nwarps;
-    cw = c0 * per;
-    whi = cw + per < mwords ? cw + per : mwords;
-  }
-  const int pf = MASK ? 0 : d.tune_pf;
+  const int pf = d.tune_pf;
   // DEFER: locks of ops finished in a warp's last round of a chunk are
   // released after the NEXT chunk's first tag loads are issued, behind the
   // one fence that also orders those loads -- the fence's wait for this
@@ -563,34 +549,10 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
   // instead of stalling the warp on its own (ncu: membar was 31% of stalls)
   u64 rel0 = ~0ull, rel1 = ~0ull;
   for (int k = 1; k < pf; k++) prefetch_tag_block(d, keys, (c0 + k * nwarps) * 32 + lane, n);
-  for (u64 c = c0; MASK ? cw < whi : c * 32 < n; c += nwarps) {
-    u64 i = c * 32 + lane;
+  for (u64 c = c0; c * 32 < n; c += nwarps) {
+    const u64 i = c * 32 + lane;
     if (pf) prefetch_tag_block(d, keys, (c + pf * nwarps) * 32 + lane, n);
     bool pending = i < n;
-    if constexpr (MASK) {
-      const u64 wi = cw + lane;
-      const u32 bits = wi < whi ? __ldg(dmask + wi) : 0u;
-      const u32 cnt = __popc(bits);
-      u32 incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const u32 t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const int k = __popc(__ballot_sync(0xFFFFFFFFu, incl <= 32));  // whole words, <= 32 ops
-      const u32 total = __shfl_sync(0xFFFFFFFFu, incl, k - 1);
-      u64* mp = mpos[(threadIdx.x >> 5) & 7];
-      if (lane < k) {
-        u32 o = incl - cnt;
-        for (u32 b = bits; b; b &= b - 1) mp[o++] = wi * 32 + (__ffs(b) - 1);
-      }
-      __syncwarp();
-      pending = (u32)lane < total;
-      i = pending ? mp[lane] : 0;
-      __syncwarp();
-      cw += k;
-    }
-    const bool mine = pending;
     u64 key = 0, val = 0, b0 = 0, b1 = 0;
     u16 tag = 1;
     if (pending) {
@@ -739,7 +701,7 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
         if (backoff < 4096) backoff <<= 1;
       }
     }
-    if (status && (MASK ? mine : i < n)) status[i] = st;
+    if (status && i < n) status[i] = st;
   }
   if (DEFER && !PHASED && __any_sync(0xFFFFFFFFu, rel0 != ~0ull || rel1 != ~0ull)) {
     fence_acq_rel();

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kThreads) k_ops(Dev d, const u8* __restrict__ 
                                                   u64* lock_acc, int conc_erase, int gated,
                                                   const u32* __restrict__ rlist = nullptr,
                                                   const u32* __restrict__ rcount = nullptr) {
-  if (gate_closed(d, gated)) return;
+  WS_PROLOGUE(d, gated, n);
   Probe* pp = nullptr;
   Probe pr;
   if constexpr (INSTR) pp = &pr;
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kThreads) k_ops(Dev d, const u8* __restrict__ 
 template <int DES, int BS, bool RO>
 __global__ void __launch_bounds__(kThreads) k_query(Dev d, const u64* __restrict__ keys, u64 n,
                                                     u64* vout, u8* found, int conc_erase, int gated) {
-  if (gate_closed(d, gated)) return;
+  WS_PROLOGUE(d, gated, n);
   Ctx<DES, BS, RO, false> c{d, nullptr, conc_erase != 0, ld_u32_relaxed(d.state)};
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     u64 v = 0;

@@ -35,6 +35,9 @@ struct Dev {
   // one table never see each other's verdicts): [0] invalid keys  [1] invalid
   // op bytes  [2] chain pool exhausted  [3] erase count of a mixed batch
   u32* cs;
+  // per-call device-resident batch size (multi-GPU exchange: the owner's
+  // inbox count is known only on the device); nullptr = the launch's n
+  const u64* dn;
   u64* chain_next;   // chaining bump allocator
   u64 chain_cap;     // physical node capacity of the arena
   u64* bfs_mem;      // cuckoo BFS workspaces
@@ -60,6 +63,14 @@ struct Dev {
   u32 delay_ns, delay_p16;
   u64 delay_seed;
 };
+
+// Kernel prologue of every batch kernel: a batch whose validation failed
+// (this call's cs words) does nothing; a device-resident batch size clamps n.
+#define WS_PROLOGUE(d, gated, n)                                                    \
+  do {                                                                              \
+    if ((gated) && (ld_u32_relaxed((d).cs) | ld_u32_relaxed((d).cs + 1))) return;   \
+    if ((d).dn) { const u64 dn_ = *(const volatile u64*)(d).dn; if (dn_ < (n)) (n) = dn_; } \
+  } while (0)
 
 __device__ __forceinline__ u64 apply_merge(int m, u64 old, u64 nv) {
   switch (m) {

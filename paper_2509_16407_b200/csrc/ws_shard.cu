@@ -10,7 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -133,39 +136,49 @@ WS_API int ws_unpermute(const void* in, const uint32_t* perm, uint64_t n, int el
 }  // extern "C"
 
 // ============================================================================
-// Fused routing over NVLink peer memory ("xchg").
+// Fused routing over NVLink peer memory ("xchg"), double-buffered.
 //
-// Every rank owns one IPC-exported region:
-//   inbox  keys / vals / src / ops   world x C entries  (segment s <- rank s)
-//   incoming[world]                   entries rank s wrote into segment s
-//   result  status / value            world x C (local results of the inbox)
-//   reply   status / value            C          (results for MY ops, written by owners)
-//   bar                               barrier counter (peers add, owner waits)
-// A round moves up to C of this rank's ops:
-//   1. k_xs_send: owner of each op, warp-aggregated position in the owner's
-//      segment `rank` (local counters: the sender owns that segment), keys /
-//      vals / op bytes / source index stored straight into the owner's inbox
-//      over NVLink; the last CTA publishes the per-owner counts into the
-//      owners' `incoming[rank]` and signals every owner's barrier
-//      (fence.sc.sys + red.release.sys).
-//   2. k_xs_wait: one thread spins (ld.acquire.sys) until world signals.
-//   3. the owner applies each inbox segment with the ordinary table kernels.
-//   4. k_xs_reply: results stored straight into the source rank's reply
-//      buffer at the op's source index; last CTA signals, 5. wait.
-// No partition buffer, no all-to-all call, no unpermute pass.
+// Every rank owns one IPC-exported region holding TWO buffers b = 0, 1:
+//   inbox[b]     keys / vals / src / ops, world x C entries (segment s <- rank s)
+//   incoming[b]  entries rank s wrote into segment s of round r's inbox
+//   result[b]    status / value of the inbox entries (applied locally)
+//   reply[b]     status / value for MY ops of the round, written by owners
+//   bar_send[b], bar_rep[b]   monotonic arrival counters (peers add, I wait)
+// Round r uses buffer b = r & 1 and moves up to C of this rank's ops:
+//   s_send: k_xs_send routes each op into its owner's inbox[b] segment
+//           `rank` over NVLink (warp-aggregated LOCAL reservations: a sender
+//           owns its segment in every inbox); the last CTA publishes the
+//           per-owner counts and signals every owner's bar_send[b]
+//           (fence.sc.sys + red.release.sys)
+//   s:      k_xs_wait(bar_send[b]) -> one table launch per inbox segment with
+//           the segment's count read ON THE DEVICE (Dev::dn) -> k_xs_reply
+//           stores every result into its source's reply[b] and signals it
+//   s_recv: k_xs_wait(bar_rep[b]) -> copy reply[b] to the caller's outputs
+// No host synchronisation inside the loop.  The next round's routing runs on
+// s_send (high priority) while this round's inbox is being applied on s:
+// round r+1 only waits for the replies of round r-1 (buffer reuse), so the
+// NVLink transfer of one round hides under the local apply of the previous.
+// Waits are bounded by %globaltimer (a dead peer yields WS_ERR_TIMEOUT, never
+// a hung GPU); the timeout flag is sticky for the whole call and every later
+// wait returns at once once it is set.
 // ============================================================================
 
 struct ws_table;
 int ws_internal_run(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
-                    u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, bool query_only);
+                    u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, bool query_only,
+                    const u64* n_dev);
 
 namespace {
 
 constexpr int kMaxWorld = 8;
 constexpr u64 kWaitLimitNs = 60ull * 1000 * 1000 * 1000;  // a peer silent for 60 s is gone
 
-struct XRegion {  // byte offsets inside a rank's region
-  u64 keys, vals, src, ops, incoming, res_st, res_vo, rep_st, rep_vo, bar, total;
+struct XBuf {  // byte offsets of one buffer inside a rank's region
+  u64 keys, vals, src, ops, incoming, res_st, res_vo, rep_st, rep_vo, bar_send, bar_rep;
+};
+struct XRegion {
+  XBuf b[2];
+  u64 total;
 };
 
 XRegion layout(int world, u64 C) {
@@ -173,16 +186,20 @@ XRegion layout(int world, u64 C) {
   u64 o = 0;
   auto take = [&](u64 bytes) { const u64 at = o; o += (bytes + 255) & ~255ull; return at; };
   const u64 E = (u64)world * C;
-  r.keys = take(8 * E);
-  r.vals = take(8 * E);
-  r.src = take(4 * E);
-  r.ops = take(E);
-  r.incoming = take(8 * kMaxWorld);
-  r.res_st = take(E);
-  r.res_vo = take(8 * E);
-  r.rep_st = take(C);
-  r.rep_vo = take(8 * C);
-  r.bar = take(8);
+  for (int b = 0; b < 2; b++) {
+    XBuf& x = r.b[b];
+    x.keys = take(8 * E);
+    x.vals = take(8 * E);
+    x.src = take(4 * E);
+    x.ops = take(E);
+    x.incoming = take(8 * kMaxWorld);
+    x.res_st = take(E);
+    x.res_vo = take(8 * E);
+    x.rep_st = take(C);
+    x.rep_vo = take(8 * C);
+    x.bar_send = take(8);
+    x.bar_rep = take(8);
+  }
   r.total = o;
   return r;
 }
@@ -190,6 +207,10 @@ XRegion layout(int world, u64 C) {
 struct XPeers {
   char* base[kMaxWorld];
 };
+
+// scratch words (u32) of a rank: per buffer b at 16*b: [0, world) send
+// counters, [8] send CTAs done, [9] reply CTAs done; [32] sticky timeout flag
+constexpr int kTimeoutWord = 32;
 
 __device__ __forceinline__ void red_add_release_sys(u64* p, u64 v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
@@ -200,10 +221,11 @@ __device__ __forceinline__ u64 ld_acquire_sys(const u64* p) {
   return r;
 }
 
-// routing of this round's ops [lo, lo+m) of the local batch
-__global__ void k_xs_send(XPeers peers, XRegion L, int world, int rank, int shift, u64 C, u64 seed0,
-                          const u64* __restrict__ keys, const u64* __restrict__ vals, const u8* __restrict__ ops,
-                          u8 uop, u64 lo, u64 m, u32* cnt, u32* done_ctas) {
+// routing of this round's ops [lo, lo+m) of the local batch into buffer B of the owners
+__global__ void __launch_bounds__(256) k_xs_send(XPeers peers, XBuf B, int world, int rank, int shift, u64 C,
+                                                 u64 seed0, const u64* __restrict__ keys,
+                                                 const u64* __restrict__ vals, const u8* __restrict__ ops, u8 uop,
+                                                 u64 lo, u64 m, u32* cnt, u32* done_ctas) {
   const int lane = threadIdx.x & 31;
   for (u64 base = blockIdx.x * (u64)blockDim.x; base < m; base += (u64)gridDim.x * blockDim.x) {
     const u64 j = base + threadIdx.x;
@@ -228,10 +250,10 @@ __global__ void k_xs_send(XPeers peers, XRegion L, int world, int rank, int shif
     if (act) {
       char* R = peers.base[o];
       const u64 e = (u64)rank * C + pos;
-      ((u64*)(R + L.keys))[e] = key;
-      ((u64*)(R + L.vals))[e] = vals ? __ldg(vals + lo + j) : 0ull;
-      ((u32*)(R + L.src))[e] = (u32)j;
-      R[L.ops + e] = ops ? __ldg(ops + lo + j) : uop;
+      ((u64*)(R + B.keys))[e] = key;
+      ((u64*)(R + B.vals))[e] = vals ? __ldg(vals + lo + j) : 0ull;
+      ((u32*)(R + B.src))[e] = (u32)j;
+      R[B.ops + e] = ops ? __ldg(ops + lo + j) : uop;
     }
   }
   // last CTA out: publish counts into every owner and signal its barrier.
@@ -245,14 +267,15 @@ __global__ void k_xs_send(XPeers peers, XRegion L, int world, int rank, int shif
     const int w = threadIdx.x;
     __threadfence_system();
     char* R = peers.base[w];
-    ((volatile u64*)(R + L.incoming))[rank] = cnt[w];
+    ((volatile u64*)(R + B.incoming))[rank] = cnt[w];
     __threadfence_system();
-    red_add_release_sys((u64*)(R + L.bar), 1ull);
+    red_add_release_sys((u64*)(R + B.bar_send), 1ull);
   }
 }
 
 // Bounded device-side wait: a rank that never arrives (crashed peer) must not
 // hang the GPU; after `limit_ns` the kernel records a timeout and returns.
+// The flag is sticky for the call: once set, every later wait returns at once.
 __device__ __forceinline__ u64 globaltimer_ns() {
   u64 t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -262,6 +285,7 @@ __global__ void k_xs_wait(u64* bar, u64 target, u64 limit_ns, u32* timed_out) {
   unsigned ns = 32;
   const u64 t0 = globaltimer_ns();
   while (ld_acquire_sys(bar) < target) {
+    if (*(volatile u32*)timed_out) return;
     __nanosleep(ns);
     if (ns < 1024) ns <<= 1;
     if (globaltimer_ns() - t0 > limit_ns) {
@@ -271,20 +295,23 @@ __global__ void k_xs_wait(u64* bar, u64 target, u64 limit_ns, u32* timed_out) {
   }
 }
 
-// results of inbox segment s (n_s entries) back to rank s's reply buffer
-__global__ void k_xs_reply(XPeers peers, XRegion L, int world, u64 C, const u64* incoming_counts,
-                           char* self, u32* done_ctas, int with_vals) {
-  const u64 E = (u64)world * C;
-  const u32* src = (const u32*)(self + L.src);
-  const u8* st = (const u8*)(self + L.res_st);
-  const u64* vo = (const u64*)(self + L.res_vo);
-  for (u64 e = blockIdx.x * (u64)blockDim.x + threadIdx.x; e < E; e += (u64)gridDim.x * blockDim.x) {
-    const u64 s = e / C, j = e % C;
-    if (j >= incoming_counts[s]) continue;
+// results of inbox segment s (incoming[s] entries) back to rank s's reply buffer
+__global__ void __launch_bounds__(256) k_xs_reply(XPeers peers, XBuf B, int world, u64 C, const char* self,
+                                                  u32* done_ctas, int with_vals) {
+  const u64* incoming = (const u64*)(self + B.incoming);
+  const u32* src = (const u32*)(self + B.src);
+  const u8* st = (const u8*)(self + B.res_st);
+  const u64* vo = (const u64*)(self + B.res_vo);
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (int s = 0; s < world; s++) {
+    const u64 ns = incoming[s] < C ? incoming[s] : C;
     char* R = peers.base[s];
-    const u32 i = src[e];
-    R[L.rep_st + i] = st[e];
-    if (with_vals) ((u64*)(R + L.rep_vo))[i] = vo[e];
+    for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < ns; j += stride) {
+      const u64 e = (u64)s * C + j;
+      const u32 i = src[e];
+      R[B.rep_st + i] = st[e];
+      if (with_vals) ((u64*)(R + B.rep_vo))[i] = vo[e];
+    }
   }
   __threadfence_system();
   __syncthreads();
@@ -293,7 +320,7 @@ __global__ void k_xs_reply(XPeers peers, XRegion L, int world, u64 C, const u64*
   __syncthreads();
   if (last && threadIdx.x < (unsigned)world) {
     __threadfence_system();
-    red_add_release_sys((u64*)(peers.base[threadIdx.x] + L.bar), 1ull);
+    red_add_release_sys((u64*)(peers.base[threadIdx.x] + B.bar_rep), 1ull);
   }
 }
 
@@ -306,9 +333,17 @@ struct ws_xchg {
   char* region;           // this rank's region (device memory, IPC-exported)
   XPeers peers;           // device-usable base of every rank's region (self included)
   bool opened[kMaxWorld];
-  u32* scratch;           // [0..world) send counters, [8] send CTAs done, [9] reply CTAs done
-  u64* h_counts;          // pinned
-  u64 epoch;              // barrier target progression
+  u32* scratch;           // see kTimeoutWord
+  u32* h_flag;            // pinned: timeout verdict
+  u64 ep_send[2], ep_rep[2];  // barrier targets per buffer (monotonic across calls)
+  cudaStream_t s_send, s_recv;
+  cudaEvent_t ev_start, ev_free[2], ev_send_done, ev_recv_done;
+  // WS_XCHG_TRACE=<file>: timing events around every phase of every round
+  // (route on s_send, apply + reply on s, reply wait + copy-out on s_recv),
+  // appended to <file> as "rank,round,phase,start_ms,end_ms" after each call
+  // -- the evidence that round r+1's routing overlaps round r's apply
+  const char* trace_path;
+  std::vector<cudaEvent_t> tev;
 };
 
 extern "C" {
@@ -327,9 +362,19 @@ WS_API int ws_xchg_create(int world, int rank, uint64_t chunk_ops, int device, w
   if (cudaMalloc((void**)&x->region, x->L.total) != cudaSuccess) { delete x; return WS_ERR_ALLOC; }
   cudaMemset(x->region, 0, x->L.total);
   if (cudaMalloc((void**)&x->scratch, 64 * 4) != cudaSuccess) { cudaFree(x->region); delete x; return WS_ERR_ALLOC; }
-  cudaMallocHost((void**)&x->h_counts, 8 * (kMaxWorld + 1));
+  cudaMemset(x->scratch, 0, 64 * 4);
+  cudaMallocHost((void**)&x->h_flag, 64);
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  // routing runs beside the previous round's table kernels: high priority,
+  // so its CTAs are scheduled as soon as SM slots free up
+  cudaStreamCreateWithPriority(&x->s_send, cudaStreamNonBlocking, hi_prio);
+  cudaStreamCreateWithFlags(&x->s_recv, cudaStreamNonBlocking);
+  for (cudaEvent_t* e : {&x->ev_start, &x->ev_free[0], &x->ev_free[1], &x->ev_send_done, &x->ev_recv_done})
+    cudaEventCreateWithFlags(e, cudaEventDisableTiming);
   for (int i = 0; i < kMaxWorld; i++) x->peers.base[i] = nullptr;
   x->peers.base[rank] = x->region;
+  x->trace_path = getenv("WS_XCHG_TRACE");
   *out = x;
   return cudaDeviceSynchronize() == cudaSuccess ? WS_OK : WS_ERR_CUDA;
 }
@@ -365,7 +410,12 @@ WS_API int ws_xchg_destroy(ws_xchg* x) {
     if (x->opened[r]) cudaIpcCloseMemHandle(x->peers.base[r]);
   cudaFree(x->region);
   cudaFree(x->scratch);
-  cudaFreeHost(x->h_counts);
+  cudaFreeHost(x->h_flag);
+  for (cudaEvent_t e : {x->ev_start, x->ev_free[0], x->ev_free[1], x->ev_send_done, x->ev_recv_done})
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t st : {x->s_send, x->s_recv})
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t e : x->tev) cudaEventDestroy(e);
   delete x;
   return WS_OK;
 }
@@ -373,7 +423,9 @@ WS_API int ws_xchg_destroy(ws_xchg* x) {
 // One batch through the sharded table: every rank calls it collectively with
 // its own batch and the same `rounds` (= ceil(max_n / chunk) over ranks).
 // op_kind: WS_OP_UPSERT / ERASE / QUERY for a uniform batch (merge in uop's
-// high nibble), or ops != NULL for a mixed batch.  Device pointers only.
+// high nibble), or ops != NULL for a mixed batch.  Device pointers only; the
+// caller validated the batch group-wide (ShardedTable._validate), so the
+// local launches run unchecked.
 WS_API int ws_xchg_run(ws_xchg* x, ws_table* local, const uint8_t* ops, uint8_t uop, const uint64_t* keys,
                        const uint64_t* vals, uint64_t n, uint64_t rounds, uint64_t seed0, uint8_t* status,
                        uint64_t* vals_out, void* stream, uint32_t flags) {
@@ -382,63 +434,99 @@ WS_API int ws_xchg_run(ws_xchg* x, ws_table* local, const uint8_t* ops, uint8_t 
   cudaStream_t s = (cudaStream_t)stream;
   const int W = x->world, log2w = __builtin_ctz((unsigned)W);
   const int shift = log2w ? 64 - log2w : 64;
-  const XRegion& L = x->L;
   const bool mixed = ops != nullptr;
   const int kind = uop & 15;
   const bool q_only = !mixed && kind == OP_QUERY;
   const bool has_erase = mixed || kind == OP_ERASE;
   const bool has_upsert = mixed || kind == OP_UPSERT;
   const bool want_vals = mixed || q_only;
+  const u32 lflags = (flags & ~(WS_F_SYNC_CHECK | WS_F_COMBINE)) | WS_F_NO_CHECK;
+  u32* tflag = x->scratch + kTimeoutWord;
+#define XCK(call) do { if ((call) != cudaSuccess) return WS_ERR_CUDA; } while (0)
+  // tracing: 6 timing events per round (send a/b, apply a/b, recv a/b) + t0
+  const bool tr = x->trace_path != nullptr;
+  if (tr) {
+    while (x->tev.size() < 1 + 6 * rounds) {
+      cudaEvent_t e;
+      XCK(cudaEventCreate(&e));
+      x->tev.push_back(e);
+    }
+    XCK(cudaEventRecord(x->tev[0], s));
+  }
+  auto mark = [&](u64 r, int k, cudaStream_t st) { if (tr) cudaEventRecord(x->tev[1 + 6 * r + k], st); };
+  // the call starts after everything already queued on the caller's stream
+  XCK(cudaMemsetAsync(tflag, 0, 4, s));
+  XCK(cudaEventRecord(x->ev_start, s));
+  XCK(cudaStreamWaitEvent(x->s_send, x->ev_start, 0));
+  XCK(cudaStreamWaitEvent(x->s_recv, x->ev_start, 0));
   int rc = WS_OK;
   for (u64 r = 0; r < rounds && rc == WS_OK; r++) {
+    const int b = (int)(r & 1);
+    const XBuf& B = x->L.b[b];
     const u64 lo = r * x->C;
     const u64 m = lo < n ? std::min<u64>(x->C, n - lo) : 0;
-    // 1. route this round's ops into the owners' inboxes
-    if (cudaMemsetAsync(x->scratch, 0, 64 * 4, s) != cudaSuccess) return WS_ERR_CUDA;
-    u64 g = (m + 255) / 256;
-    g = std::max<u64>(1, std::min<u64>(g, 148 * 4));
-    k_xs_send<<<(unsigned)g, 256, 0, s>>>(x->peers, L, W, x->rank, shift, x->C, seed0, (const u64*)keys,
-                                          (const u64*)vals, ops, uop, lo, m, x->scratch, x->scratch + 8);
-    x->epoch += W;
-    k_xs_wait<<<1, 1, 0, s>>>((u64*)(x->region + L.bar), x->epoch, kWaitLimitNs, x->scratch + 10);
-    // 2. apply each source segment locally
-    if (cudaMemcpyAsync(x->h_counts, x->region + L.incoming, 8 * W, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return WS_ERR_CUDA;
-    if (cudaMemcpyAsync(x->h_counts + kMaxWorld, x->scratch + 10, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-      return WS_ERR_CUDA;
-    if (cudaStreamSynchronize(s) != cudaSuccess) return WS_ERR_CUDA;
-    if (*(const u32*)(x->h_counts + kMaxWorld)) return WS_ERR_TIMEOUT;
+    u32* sc = x->scratch + 16 * b;
+    // 1. [s_send] route this round's ops once every owner has released buffer b
+    //    (= my replies of round r-2 arrived, recorded on s_recv)
+    if (r >= 2) XCK(cudaStreamWaitEvent(x->s_send, x->ev_free[b], 0));
+    XCK(cudaMemsetAsync(sc, 0, 16 * 4, x->s_send));
+    const u64 g = std::max<u64>(1, std::min<u64>((m + 255) / 256, 148 * 2));
+    mark(r, 0, x->s_send);
+    k_xs_send<<<(unsigned)g, 256, 0, x->s_send>>>(x->peers, B, W, x->rank, shift, x->C, seed0, (const u64*)keys,
+                                                  (const u64*)vals, ops, uop, lo, m, sc, sc + 8);
+    mark(r, 1, x->s_send);
+    // 2. [s] wait for every source's segment, apply each segment with its
+    //    device-resident count, return the results
+    x->ep_send[b] += W;
+    k_xs_wait<<<1, 1, 0, s>>>((u64*)(x->region + B.bar_send), x->ep_send[b], kWaitLimitNs, tflag);
+    const u64* inc = (const u64*)(x->region + B.incoming);
+    mark(r, 2, s);
     for (int src = 0; src < W && rc == WS_OK; src++) {
-      const u64 ns = x->h_counts[src];
-      if (!ns) continue;
       const u64 e = (u64)src * x->C;
-      rc = ws_internal_run(local, mixed ? (const u8*)(x->region + L.ops) + e : nullptr, uop,
-                           (const u64*)(x->region + L.keys) + e,
-                           has_upsert ? (const u64*)(x->region + L.vals) + e : nullptr, ns,
-                           (u8*)(x->region + L.res_st) + e, want_vals ? (u64*)(x->region + L.res_vo) + e : nullptr,
-                           s, flags, has_erase, has_upsert, q_only);
+      rc = ws_internal_run(local, mixed ? (const u8*)(x->region + B.ops) + e : nullptr, uop,
+                           (const u64*)(x->region + B.keys) + e,
+                           has_upsert ? (const u64*)(x->region + B.vals) + e : nullptr, x->C,
+                           (u8*)(x->region + B.res_st) + e, want_vals ? (u64*)(x->region + B.res_vo) + e : nullptr,
+                           s, lflags, has_erase, has_upsert, q_only, inc + src);
     }
     if (rc) break;
-    // 3. return results to their sources, 4. wait for mine
-    k_xs_reply<<<148 * 4, 256, 0, s>>>(x->peers, L, W, x->C, (const u64*)(x->region + L.incoming), x->region,
-                                       x->scratch + 9, want_vals ? 1 : 0);
-    x->epoch += W;
-    k_xs_wait<<<1, 1, 0, s>>>((u64*)(x->region + L.bar), x->epoch, kWaitLimitNs, x->scratch + 10);
+    k_xs_reply<<<148 * 2, 256, 0, s>>>(x->peers, B, W, x->C, x->region, sc + 9, want_vals ? 1 : 0);
+    mark(r, 3, s);
+    // 3. [s_recv] wait for my replies, copy them out, release buffer b
+    x->ep_rep[b] += W;
+    mark(r, 4, x->s_recv);
+    k_xs_wait<<<1, 1, 0, x->s_recv>>>((u64*)(x->region + B.bar_rep), x->ep_rep[b], kWaitLimitNs, tflag);
     if (m) {
-      if (status && cudaMemcpyAsync(status + lo, x->region + L.rep_st, m, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-        return WS_ERR_CUDA;
-      if (vals_out && cudaMemcpyAsync(vals_out + lo, x->region + L.rep_vo, 8 * m, cudaMemcpyDeviceToDevice, s) !=
-                          cudaSuccess)
-        return WS_ERR_CUDA;
+      if (status) XCK(cudaMemcpyAsync(status + lo, x->region + B.rep_st, m, cudaMemcpyDeviceToDevice, x->s_recv));
+      if (vals_out)
+        XCK(cudaMemcpyAsync(vals_out + lo, x->region + B.rep_vo, 8 * m, cudaMemcpyDeviceToDevice, x->s_recv));
+    }
+    mark(r, 5, x->s_recv);
+    XCK(cudaEventRecord(x->ev_free[b], x->s_recv));
+  }
+  // the caller's stream resumes after every route, apply and copy-out
+  XCK(cudaEventRecord(x->ev_send_done, x->s_send));
+  XCK(cudaEventRecord(x->ev_recv_done, x->s_recv));
+  XCK(cudaStreamWaitEvent(s, x->ev_send_done, 0));
+  XCK(cudaStreamWaitEvent(s, x->ev_recv_done, 0));
+  if (rc == WS_OK && cudaGetLastError() != cudaSuccess) rc = WS_ERR_CUDA;
+  XCK(cudaMemcpyAsync(x->h_flag, tflag, 4, cudaMemcpyDeviceToHost, s));
+  XCK(cudaStreamSynchronize(s));
+  if (rc == WS_OK && *x->h_flag) rc = WS_ERR_TIMEOUT;
+  if (tr && rc == WS_OK) {
+    if (FILE* f = fopen(x->trace_path, "a")) {
+      static const char* names[3] = {"route", "apply+reply", "recv+copy"};
+      for (u64 r = 0; r < rounds; r++)
+        for (int k = 0; k < 3; k++) {
+          float a = 0, e = 0;
+          cudaEventElapsedTime(&a, x->tev[0], x->tev[1 + 6 * r + 2 * k]);
+          cudaEventElapsedTime(&e, x->tev[0], x->tev[1 + 6 * r + 2 * k + 1]);
+          fprintf(f, "%d,%llu,%s,%.4f,%.4f\n", x->rank, (unsigned long long)r, names[k], a, e);
+        }
+      fclose(f);
     }
   }
-  if (rc == WS_OK && cudaGetLastError() != cudaSuccess) rc = WS_ERR_CUDA;
-  if (rc == WS_OK) {
-    if (cudaMemcpyAsync(x->h_counts + kMaxWorld, x->scratch + 10, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
-      return WS_ERR_CUDA;
-    if (*(const u32*)(x->h_counts + kMaxWorld)) rc = WS_ERR_TIMEOUT;
-  }
+#undef XCK
   return rc;
 }
 

@@ -601,21 +601,13 @@ class HashTable:
         return {"slot_engine": self.slot_engine, "wide_atomic": True,
                 "device": f"cuda:{self.device.index}", "arch": "sm_100a"}
 
-    def tune(self, query_ilp=None, l2_policy=None, upsert=None, occupancy=None, bulk=None,
-             bulk_group=None, prefetch=None):
+    def tune(self, query_ilp=None, l2_policy=None, upsert=None, occupancy=None, prefetch=None):
         """Performance knobs of the tuned P2-MD path (no semantic effect).
 
         prefetch: L2 prefetch distance (grid-stride iterations) of the primary
-        tag block in the tuned P2-MD upsert / query kernels, 0 = off;
-        bulk: bucket-partitioned bulk upsert (csrc/ws_bulk.cu) -- 0 off,
-        1 auto (large uniform upsert batches), 2 whenever eligible;
-        bulk_group: log2 buckets per owner group (-1 = from batch density)."""
+        tag block in the tuned P2-MD upsert / query kernels, 0 = off."""
         if prefetch is not None:
             self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_PREFETCH, int(prefetch)))
-        if bulk is not None:
-            self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_BULK, int(bulk)))
-        if bulk_group is not None:
-            self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_BULK_GROUP, int(bulk_group)))
         if occupancy is not None:
             self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_OCCUPANCY, int(occupancy)))
         if upsert is not None:
