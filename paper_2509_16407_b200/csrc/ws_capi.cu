@@ -360,6 +360,9 @@ __global__ void k_seg_starts(const u8* __restrict__ op_sorted, u64 n, u64* start
 // queries through the lock-free query kernel -- one after another on the
 // stream, then the results are scattered back.  Running the segments in
 // sequence is one serial order of the concurrent batch.
+int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status, cudaStream_t s,
+                    u32 flags, const CallCtx& cx);
+
 int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
                        u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, const CallCtx& cx) {
   int rc = validate(keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
@@ -388,6 +391,7 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
   std::vector<u64> st_h(256);
   if (!rc) rc = cuda_err(cudaMemcpyAsync(st_h.data(), starts, 8 * 256, cudaMemcpyDeviceToHost, s));
   if (!rc) rc = cuda_err(cudaStreamSynchronize(s));
+  const bool comb = (flags & WS_F_COMBINE) != 0;
   const u32 inner = (flags & ~(WS_F_SYNC_CHECK | WS_F_COMBINE)) | kF_NO_KIND_SORT |
                     ((flags & WS_F_NO_CHECK) ? 0u : (kF_VALIDATED | WS_F_NO_CHECK));
   // segments in op-byte order
@@ -401,8 +405,9 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
     const int kind = v & 15, merge = v >> 4;
     const u64 m = hi - lo;
     if (kind == OP_UPSERT && merge <= M_MIN && v_p) {
-      rc = run_device_plain(t, nullptr, v, k_p + lo, v_p + lo, m, st_p + lo, nullptr, s, inner, false, true, false,
-                            cx);
+      rc = comb && m >= 2 ? combine_uniform(t, v, k_p + lo, v_p + lo, m, st_p + lo, s, inner, cx)
+                          : run_device_plain(t, nullptr, v, k_p + lo, v_p + lo, m, st_p + lo, nullptr, s, inner,
+                                             false, true, false, cx);
       if (vo_p && !rc) rc = cuda_err(cudaMemsetAsync(vo_p + lo, 0, 8 * m, s));
     } else if (kind == OP_ERASE && merge == 0) {
       rc = run_device_plain(t, nullptr, v, k_p + lo, nullptr, m, st_p + lo, nullptr, s, inner, true, false, false,
@@ -487,11 +492,20 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
 
 // ------------------------------------------------------------------ combining
 // WS_F_COMBINE: same-key upserts of one batch are reduced before they touch
-// the table (radix sort by key, runs of equal (key, op byte) folded with the
-// op's merge), one op per run is applied, and statuses are expanded: the run
-// leader gets the real status, other members UPDATED (FULL if the leader was).
-// Equivalent to some serial order of the batch for every merge; the point is
-// Zipf hot keys, whose ops would otherwise serialise on one bucket lock.
+// the table; one op per (key, merge) group is applied and the statuses are
+// expanded: the group leader gets the real status, the other members
+// UPDATED (FULL if the leader was).  Equivalent to a serial order of the
+// batch in which each group's upserts run back to back; the point is Zipf
+// hot keys, whose ops would otherwise serialise on one bucket lock.
+//   * mixed batches are first split by op byte (run_device_by_kind); every
+//     upsert segment (one merge) is then combined on its own;
+//   * commutative merges (ADD / MAX / MIN): hash aggregation into an
+//     L2-resident open-addressing table (claim by CAS, fold by one atomic
+//     per op), compaction of the occupied slots, apply with the group count
+//     read on the device -- no sort and no host synchronisation;
+//   * REPLACE / KEEP: a stable 64-bit key sort keeps batch-index order inside
+//     each key's run, so the fold reproduces the index order (last REPLACE /
+//     first KEEP wins, as the sequential reference would).
 struct OpVal {
   u64 v;
   u32 op;
@@ -506,217 +520,211 @@ struct CombineOp {
   }
 };
 
-__device__ __forceinline__ u8 op_at(const u8* ops, u8 uop, u64 i) { return ops ? ops[i] : uop; }
-
 __global__ void k_comb_iota(u64 n, u32* idx) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) idx[i] = (u32)i;
 }
 
-__global__ void k_comb_gather(const u64* keys, const u32* order, u64 n, u64* out) {
+__global__ void k_comb_heads(const u64* sk, const u32* si, u8 uop, const u64* vals, u64 n, u32* head, OpVal* ov) {
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
+    head[j] = j == 0 || sk[j] != sk[j - 1];
+    ov[j] = OpVal{vals ? vals[si[j]] : 0ull, uop, 0};
+  }
+}
+
+__global__ void k_comb_groups(const u64* sk, const u32* head, const u32* seg, u64 n, u64* gkey) {
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x)
-    out[j] = keys[order[j]];
+    if (head[j]) gkey[seg[j] - 1] = sk[j];
 }
 
-// [lo, hi) of the positions holding upserts in an op-byte-sorted batch
-__global__ void k_upsert_range(const u8* op_sorted, u64 n, u32* lohi) {
-  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
-    const bool up = (op_sorted[j] & 15) == OP_UPSERT;
-    const bool first = up && (j == 0 || (op_sorted[j - 1] & 15) != OP_UPSERT);
-    const bool last = up && (j + 1 == n || (op_sorted[j + 1] & 15) != OP_UPSERT);
-    if (first) atomicMin(lohi, (u32)j);
-    if (last) atomicMax(lohi + 1, (u32)(j + 1));
-    const int m = op_sorted[j] >> 4;
-    // any upsert with an order-sensitive merge (REPLACE / KEEP) rules out the
-    // hash sort for the whole span; warp-aggregated, one atomic per warp
-    const bool ord = up && m != M_ADD && m != M_MAX && m != M_MIN;
-    const unsigned am = __activemask();
-    const unsigned any = __ballot_sync(am, ord);
-    if (any && (threadIdx.x & 31) == (unsigned)(__ffs(am) - 1)) atomicOr(lohi + 2, 1u);
-  }
-}
-
-// 32-bit sort key for commutative combining: the high half of mix64(key)
-__global__ void k_comb_hash32(const u64* keys, u64 n, u32* h) {
-  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
-    h[i] = (u32)(mix64(keys[i]) >> 32);
-}
-
-__global__ void k_comb_heads(const u64* sk, const u32* si, const u8* ops, u8 uop, const u64* vals, u64 n,
-                             u32* head, OpVal* ov) {
-  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
-    const u8 op = op_at(ops, uop, si[j]);
-    bool h = j == 0 || (op & 15) != OP_UPSERT;
-    if (!h) h = sk[j] != sk[j - 1] || op_at(ops, uop, si[j - 1]) != op;
-    head[j] = h;
-    ov[j] = OpVal{vals ? vals[si[j]] : 0ull, op, 0};
-  }
-}
-
-__global__ void k_comb_groups(const u64* sk, const u32* si, const u32* head, const u32* seg, const u8* ops, u8 uop,
-                              u64 n, u64* gkey, u8* gop) {
-  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
-    if (!head[j]) continue;
-    const u32 g = seg[j] - 1;
-    gkey[g] = sk[j];
-    gop[g] = op_at(ops, uop, si[j]);
-  }
-}
-
-__global__ void k_comb_vals(const OpVal* agg, u64 ng, u64* gval) {
-  for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < ng; g += (u64)gridDim.x * blockDim.x)
+__global__ void k_comb_vals(const OpVal* agg, const u64* ng, u64 n, u64* gval) {
+  const u64 m = *ng < n ? *ng : n;
+  for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < m; g += (u64)gridDim.x * blockDim.x)
     gval[g] = agg[g].v;
 }
 
-__global__ void k_comb_expand(const u32* si, const u32* head, const u32* seg, u64 n, const u8* gst, const u64* gvo,
-                              u8* status, u64* vout) {
+__global__ void k_comb_expand(const u32* si, const u32* head, const u32* seg, u64 n, const u8* gst, u8* status) {
   for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
-    const u32 g = seg[j] - 1;
-    const u32 i = si[j];
-    const u8 gs = gst[g];
-    if (status) status[i] = head[j] ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
-    if (vout) vout[i] = head[j] ? gvo[g] : 0ull;
+    const u8 gs = gst[seg[j] - 1];
+    status[si[j]] = head[j] ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
   }
+}
+
+// hash aggregation of one commutative-merge upsert batch.  Lanes of a warp
+// holding the same key fold their values first (__match_any_sync), so a Zipf
+// hot key costs one table atomic per warp instead of one per op.
+__device__ __forceinline__ u64 merge_of(int merge, u64 a, u64 b) {
+  return merge == M_ADD ? a + b : merge == M_MAX ? (a > b ? a : b) : (a < b ? a : b);
+}
+__global__ void __launch_bounds__(256) k_agg_insert(const u64* __restrict__ keys, const u64* __restrict__ vals,
+                                                    u64 n, int merge, u64* tk, u64* tv, u32* leader, u64 mask,
+                                                    u32* grp) {
+  const int lane = threadIdx.x & 31;
+  for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n;
+       base += (u64)gridDim.x * blockDim.x) {
+    const u64 i = base + lane;
+    const bool act = i < n;
+    const u64 key = act ? __ldg(keys + i) : 0ull;
+    u64 v = act ? __ldg(vals + i) : 0ull;
+    const unsigned act_m = __ballot_sync(0xFFFFFFFFu, act);
+    const unsigned same = __match_any_sync(0xFFFFFFFFu, key) & act_m;
+    const int first = __ffs(same) - 1;
+    // fold the group's values into its first lane (all lanes take part in every shuffle)
+    for (int j = 0; j < 32; j++) {
+      const u64 vj = __shfl_sync(0xFFFFFFFFu, v, j);
+      if (act && lane == first && j != lane && ((same >> j) & 1u)) v = merge_of(merge, v, vj);
+    }
+    u64 h = 0;
+    if (act && lane == first) {
+      h = mix64(key ^ 0x9E3779B97F4A7C15ull) & mask;
+      while (true) {
+        const u64 cur = *(volatile const u64*)(tk + h);
+        if (cur == key) break;
+        if (cur == 0) {
+          const u64 prev = atomicCAS((unsigned long long*)(tk + h), 0ull, (unsigned long long)key);
+          if (prev == 0 || prev == key) break;
+        }
+        h = (h + 1) & mask;
+      }
+      // the group's leader (the op that reports INSERTED for a new key) is its
+      // lowest batch index, as in the sequential reference order; the first
+      // lane of a warp group holds the group's lowest index
+      atomicMin(leader + h, (u32)i);
+      if (merge == M_ADD) atomicAdd((unsigned long long*)(tv + h), (unsigned long long)v);
+      else if (merge == M_MAX) atomicMax((unsigned long long*)(tv + h), (unsigned long long)v);
+      else atomicMin((unsigned long long*)(tv + h), (unsigned long long)v);
+    }
+    h = __shfl_sync(0xFFFFFFFFu, h, first < 0 ? 0 : first);
+    if (act) grp[i] = (u32)h;
+  }
+}
+
+// one group per leader op (ops, not table slots, are scanned)
+__global__ void __launch_bounds__(256) k_agg_compact(const u64* __restrict__ keys, const u32* __restrict__ grp,
+                                                     const u32* leader, const u64* tv, u64 n, u64* gkey, u64* gval,
+                                                     u32* slot2g, u64* ng) {
+  const int lane = threadIdx.x & 31;
+  for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n;
+       base += (u64)gridDim.x * blockDim.x) {
+    const u64 i = base + lane;
+    const u32 h = i < n ? grp[i] : 0u;
+    const bool lead = i < n && leader[h] == (u32)i;
+    const u32 m = __ballot_sync(0xFFFFFFFFu, lead);
+    if (!m) continue;
+    u64 at = 0;
+    if (lane == 0) at = atomicAdd((unsigned long long*)ng, (unsigned long long)__popc(m));
+    at = __shfl_sync(0xFFFFFFFFu, at, 0);
+    if (lead) {
+      const u64 g = at + __popc(m & ((1u << lane) - 1));
+      gkey[g] = __ldg(keys + i);
+      gval[g] = tv[h];
+      slot2g[h] = (u32)g;
+    }
+  }
+}
+
+__global__ void k_agg_expand(const u32* grp, const u32* leader, const u32* slot2g, u64 n, const u8* gst, u8* status) {
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u32 h = grp[i];
+    const u8 gs = gst[slot2g[h]];
+    status[i] = leader[h] == (u32)i ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
+  }
+}
+
+// one uniform upsert batch (merge = uop >> 4), combined; see above
+int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status, cudaStream_t s,
+                    u32 flags, const CallCtx& cx) {
+  int rc = validate(keys, nullptr, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
+  if (rc) return rc;
+  // the folded batch keeps the kernels gated on this call's validation verdict
+  // (an asynchronous check is not read back here, but a batch holding a
+  // sentinel key still mutates nothing)
+  const u32 inner = (flags & ~(WS_F_COMBINE | WS_F_SYNC_CHECK)) | WS_F_NO_CHECK |
+                    ((flags & WS_F_NO_CHECK) && !(flags & kF_VALIDATED) ? 0u : kF_VALIDATED);
+  const int m = uop >> 4;
+  std::vector<void*> mem;
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 16, s) != cudaSuccess) return nullptr;
+    mem.push_back(p);
+    return p;
+  };
+  auto release = [&]() { for (void* p : mem) cudaFreeAsync(p, s); };
+  u8* gst = (u8*)alloc(n);
+  u64* gkey = (u64*)alloc(8 * n);
+  u64* gval = (u64*)alloc(8 * n);
+  u64* ng = (u64*)alloc(8);
+  if (!gst || !gkey || !gval || !ng) { release(); return WS_ERR_ALLOC; }
+  CallCtx gcx = cx;
+  gcx.dn = ng;  // the group count stays on the device
+  if (m == M_ADD || m == M_MAX || m == M_MIN) {
+    const u64 cap = next_pow2(n + n / 2);  // load <= 2/3; ~24 B/slot, L2-resident up to ~3M ops
+    u64* tk = (u64*)alloc(8 * cap);
+    u64* tv = (u64*)alloc(8 * cap);
+    u32* leader = (u32*)alloc(4 * cap);
+    u32* slot2g = (u32*)alloc(4 * cap);
+    u32* grp = (u32*)alloc(4 * n);
+    if (!tk || !tv || !leader || !slot2g || !grp) { release(); return WS_ERR_ALLOC; }
+    WS_CK(cudaMemsetAsync(tk, 0, 8 * cap, s));
+    WS_CK(cudaMemsetAsync(tv, m == M_MIN ? 0xFF : 0, 8 * cap, s));  // the merge's identity
+    WS_CK(cudaMemsetAsync(leader, 0xFF, 4 * cap, s));
+    WS_CK(cudaMemsetAsync(slot2g, 0, 4 * cap, s));
+    WS_CK(cudaMemsetAsync(ng, 0, 8, s));
+    k_agg_insert<<<grid_for(n), 256, 0, s>>>(keys, vals, n, m, tk, tv, leader, cap - 1, grp);
+    k_agg_compact<<<grid_for(n), 256, 0, s>>>(keys, grp, leader, tv, n, gkey, gval, slot2g, ng);
+    rc = cuda_err(cudaGetLastError());
+    if (!rc) rc = run_device_plain(t, nullptr, uop, gkey, gval, n, gst, nullptr, s, inner, false, true, false, gcx);
+    if (!rc && status) {
+      k_agg_expand<<<grid_for(n), kThreads, 0, s>>>(grp, leader, slot2g, n, gst, status);
+      rc = cuda_err(cudaGetLastError());
+    }
+    release();
+    return rc;
+  }
+  // REPLACE / KEEP: stable key sort, runs folded in index order
+  u64* sk = (u64*)alloc(8 * n);
+  u32* idx = (u32*)alloc(4 * n);
+  u32* si = (u32*)alloc(4 * n);
+  u32* head = (u32*)alloc(4 * n);
+  u32* seg = (u32*)alloc(4 * n);
+  u32* uniq = (u32*)alloc(4 * n);
+  OpVal* ov = (OpVal*)alloc(sizeof(OpVal) * n);
+  OpVal* agg = (OpVal*)alloc(sizeof(OpVal) * n);
+  if (!sk || !idx || !si || !head || !seg || !uniq || !ov || !agg) { release(); return WS_ERR_ALLOC; }
+  size_t tb = 0, tb2 = 0, tb3 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
+  cub::DeviceScan::InclusiveSum(nullptr, tb2, head, seg, (int64_t)n, s);
+  cub::DeviceReduce::ReduceByKey(nullptr, tb3, seg, uniq, ov, agg, ng, CombineOp(), (int64_t)n, s);
+  void* tmp = alloc(std::max(tb, std::max(tb2, tb3)) + 16);
+  if (!tmp) { release(); return WS_ERR_ALLOC; }
+  k_comb_iota<<<grid_for(n), kThreads, 0, s>>>(n, idx);
+  cub::DeviceRadixSort::SortPairs(tmp, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
+  k_comb_heads<<<grid_for(n), kThreads, 0, s>>>(sk, si, uop, vals, n, head, ov);
+  cub::DeviceScan::InclusiveSum(tmp, tb2, head, seg, (int64_t)n, s);
+  cub::DeviceReduce::ReduceByKey(tmp, tb3, seg, uniq, ov, agg, ng, CombineOp(), (int64_t)n, s);
+  k_comb_groups<<<grid_for(n), kThreads, 0, s>>>(sk, head, seg, n, gkey);
+  k_comb_vals<<<grid_for(n), kThreads, 0, s>>>(agg, ng, n, gval);
+  rc = cuda_err(cudaGetLastError());
+  if (!rc) rc = run_device_plain(t, nullptr, uop, gkey, gval, n, gst, nullptr, s, inner, false, true, false, gcx);
+  if (!rc && status) {
+    k_comb_expand<<<grid_for(n), kThreads, 0, s>>>(si, head, seg, n, gst, status);
+    rc = cuda_err(cudaGetLastError());
+  }
+  release();
+  return rc;
 }
 
 int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                bool query_only, const CallCtx& cx) {
-  if (!(flags & WS_F_COMBINE) || query_only || !has_upsert || n < 2 || n >= (1ull << 32) ||
-      (flags & WS_F_SERIAL) || cx.dn)
+  const bool comb = (flags & WS_F_COMBINE) && !query_only && has_upsert && n >= 2 && n < (1ull << 32) &&
+                    !(flags & (WS_F_SERIAL | WS_F_INTERLEAVED)) && !cx.dn && !t->d.delay_ns && vals;
+  if (!comb)
     return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s, flags & ~WS_F_COMBINE, has_erase,
                             has_upsert, query_only, cx);
-  int rc = validate(keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
-  if (rc) return rc;
-  // the folded batch keeps the kernels gated on this call's validation verdict
-  // (an asynchronous check is not read back here, but a batch holding a
-  // sentinel key or a bad op byte still mutates nothing)
-  const u32 inner = (flags & ~(WS_F_COMBINE | WS_F_SYNC_CHECK)) | WS_F_NO_CHECK |
-                    ((flags & WS_F_NO_CHECK) ? 0u : kF_VALIDATED);
-  // scratch: sorted keys / indices, heads, segment ids, op-values, groups
-  u64 *sk = nullptr, *gkey = nullptr, *gval = nullptr, *gvo = nullptr;
-  u32 *idx = nullptr, *si = nullptr, *head = nullptr, *seg = nullptr, *uniq = nullptr;
-  OpVal *ov = nullptr, *agg = nullptr;
-  u8 *gop = nullptr, *gst = nullptr;
-  u64* nruns = nullptr;
-  WS_CK(cudaMallocAsync((void**)&sk, 8 * n, s));
-  WS_CK(cudaMallocAsync((void**)&idx, 4 * n, s));
-  WS_CK(cudaMallocAsync((void**)&si, 4 * n, s));
-  WS_CK(cudaMallocAsync((void**)&head, 4 * n, s));
-  WS_CK(cudaMallocAsync((void**)&seg, 4 * n, s));
-  WS_CK(cudaMallocAsync((void**)&uniq, 4 * std::max<u64>(n, 4), s));
-  WS_CK(cudaMallocAsync((void**)&ov, sizeof(OpVal) * n, s));
-  WS_CK(cudaMallocAsync((void**)&agg, sizeof(OpVal) * n, s));
-  WS_CK(cudaMallocAsync((void**)&nruns, 8, s));
-  k_comb_iota<<<grid_for(n), kThreads, 0, s>>>(n, idx);
-  // runs must be contiguous per (key, op byte) even when a key's upserts are
-  // interleaved with other ops: for mixed batches a stable pre-sort by op
-  // byte, then a stable sort by key (LSD order) -> (key, op, index) order
-  u8 *op_sorted = nullptr;
-  u64* keys_by_op = nullptr;
-  const u64* sort_keys = keys;
-  size_t tb0 = 0, tb = 0, tb2 = 0, tb3 = 0;
-  if (ops) {
-    WS_CK(cudaMallocAsync((void**)&op_sorted, n, s));
-    WS_CK(cudaMallocAsync((void**)&keys_by_op, 8 * n, s));
-    cub::DeviceRadixSort::SortPairs(nullptr, tb0, ops, op_sorted, idx, si, (int64_t)n, 0, 8, s);
-  }
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
-  cub::DeviceScan::InclusiveSum(nullptr, tb2, head, seg, (int64_t)n, s);
-  cub::DeviceReduce::ReduceByKey(nullptr, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
-  void* tmp = nullptr;
-  const size_t tmax = std::max(std::max(tb0, tb), std::max(tb2, tb3)) + 16;
-  WS_CK(cudaMallocAsync(&tmp, tmax, s));
-  u64 lo = 0, hi = n;
-  bool span_commutative = false;
-  if (ops) {
-    // idx -> si ordered by op (stable); gather keys in that order; si -> idx
-    cub::DeviceRadixSort::SortPairs(tmp, tb0, ops, op_sorted, idx, si, (int64_t)n, 0, 8, s);
-    k_comb_gather<<<grid_for(n), kThreads, 0, s>>>(keys, si, n, keys_by_op);
-    WS_CK(cudaMemcpyAsync(idx, si, 4 * n, cudaMemcpyDeviceToDevice, s));
-    sort_keys = keys_by_op;
-    // only the upserts need key order (every other op is its own group): the
-    // 64-bit key sort covers just the span of upsert op bytes (one host read
-    // of the span; YCSB-A batch 4.2 -> 3.5 ms)
-    u32* lohi = (u32*)uniq;  // scratch until the reduce-by-key below
-    WS_CK(cudaMemsetAsync(lohi, 0xFF, 4, s));
-    WS_CK(cudaMemsetAsync(lohi + 1, 0, 8, s));
-    k_upsert_range<<<grid_for(n), kThreads, 0, s>>>(op_sorted, n, lohi);
-    u64* hp = pin();
-    if (!hp) return WS_ERR_ALLOC;
-    WS_CK(cudaMemcpyAsync(hp, lohi, 12, cudaMemcpyDeviceToHost, s));
-    WS_CK(cudaStreamSynchronize(s));
-    const u32* hl = (const u32*)hp;
-    lo = hl[0] == 0xFFFFFFFFu ? 0 : hl[0];
-    hi = hl[0] == 0xFFFFFFFFu ? 0 : hl[1];
-    span_commutative = hl[2] == 0;
-    if (hi <= lo) {
-      // no upserts at all (e.g. YCSB-C): nothing to fold -- run the batch as is
-      for (void* p : {(void*)sk, (void*)idx, (void*)si, (void*)head, (void*)seg, (void*)uniq, (void*)ov,
-                      (void*)agg, (void*)nruns, tmp, (void*)op_sorted, (void*)keys_by_op})
-        if (p) cudaFreeAsync(p, s);
-      return run_device_plain(t, ops, uop, keys, vals, n, status, vout, s, inner, has_erase, has_upsert, false, cx);
-    }
-    if (lo > 0) {
-      WS_CK(cudaMemcpyAsync(sk, keys_by_op, 8 * lo, cudaMemcpyDeviceToDevice, s));
-      WS_CK(cudaMemcpyAsync(si, idx, 4 * lo, cudaMemcpyDeviceToDevice, s));
-    }
-    if (hi < n) {
-      WS_CK(cudaMemcpyAsync(sk + hi, keys_by_op + hi, 8 * (n - hi), cudaMemcpyDeviceToDevice, s));
-      WS_CK(cudaMemcpyAsync(si + hi, idx + hi, 4 * (n - hi), cudaMemcpyDeviceToDevice, s));
-    }
-  }
-  // Uniform ADD / MAX / MIN batches sort on 32 hash bits (4 onesweep passes
-  // instead of 8).  Keys sharing the hash may interleave, so one key can form
-  // several runs; each run is folded and applied on its own, which for a
-  // commutative merge is still one serial order of the batch (one INSERTED
-  // per new key, the same final value).  REPLACE / KEEP (order-sensitive)
-  // and mixed batches keep the full 64-bit key sort.
-  const int um = uop >> 4;
-  const bool hash_sort = ops ? span_commutative : (um == M_ADD || um == M_MAX || um == M_MIN);
-  if (hash_sort && hi > lo) {
-    const u64 m = hi - lo;
-    u32 *h = nullptr, *hs = nullptr;
-    size_t tbh = 0;
-    WS_CK(cudaMallocAsync((void**)&h, 4 * m, s));
-    WS_CK(cudaMallocAsync((void**)&hs, 4 * m, s));
-    cub::DeviceRadixSort::SortPairs(nullptr, tbh, h, hs, idx + lo, si + lo, (int64_t)m, 0, 32, s);
-    void* tmph = nullptr;
-    WS_CK(cudaMallocAsync(&tmph, tbh + 16, s));
-    k_comb_hash32<<<grid_for(m), kThreads, 0, s>>>(sort_keys + lo, m, h);
-    cub::DeviceRadixSort::SortPairs(tmph, tbh, h, hs, idx + lo, si + lo, (int64_t)m, 0, 32, s);
-    k_comb_gather<<<grid_for(m), kThreads, 0, s>>>(keys, si + lo, m, sk + lo);
-    for (void* p : {(void*)h, (void*)hs, tmph}) cudaFreeAsync(p, s);
-  } else if (hi > lo) {
-    cub::DeviceRadixSort::SortPairs(tmp, tb, sort_keys + lo, sk + lo, idx + lo, si + lo, (int64_t)(hi - lo), 0, 64,
-                                    s);
-  }
-  k_comb_heads<<<grid_for(n), kThreads, 0, s>>>(sk, si, ops, uop, vals, n, head, ov);
-  cub::DeviceScan::InclusiveSum(tmp, tb2, head, seg, (int64_t)n, s);
-  cub::DeviceReduce::ReduceByKey(tmp, tb3, seg, uniq, ov, agg, nruns, CombineOp(), (int64_t)n, s);
-  u64* hp = pin();
-  if (!hp) return WS_ERR_ALLOC;
-  WS_CK(cudaMemcpyAsync(hp, nruns, 8, cudaMemcpyDeviceToHost, s));
-  WS_CK(cudaStreamSynchronize(s));
-  const u64 ng = hp[0];
-  WS_CK(cudaMallocAsync((void**)&gkey, 8 * ng, s));
-  WS_CK(cudaMallocAsync((void**)&gval, 8 * ng, s));
-  WS_CK(cudaMallocAsync((void**)&gvo, 8 * ng, s));
-  WS_CK(cudaMallocAsync((void**)&gop, ng, s));
-  WS_CK(cudaMallocAsync((void**)&gst, ng, s));
-  k_comb_groups<<<grid_for(n), kThreads, 0, s>>>(sk, si, head, seg, ops, uop, n, gkey, gop);
-  k_comb_vals<<<grid_for(ng), kThreads, 0, s>>>(agg, ng, gval);
-  WS_CK(cudaGetLastError());
-  rc = run_device_plain(t, ops ? gop : nullptr, uop, gkey, vals ? gval : nullptr, ng, gst, gvo, s, inner, has_erase,
-                        has_upsert, false, cx);
-  if (!rc) {
-    k_comb_expand<<<grid_for(n), kThreads, 0, s>>>(si, head, seg, n, gst, gvo, status, vout);
-    rc = cuda_err(cudaGetLastError());
-  }
-  for (void* p : {(void*)sk, (void*)idx, (void*)si, (void*)head, (void*)seg, (void*)uniq, (void*)ov, (void*)agg,
-                  (void*)nruns, tmp, (void*)gkey, (void*)gval, (void*)gvo, (void*)gop, (void*)gst,
-                  (void*)op_sorted, (void*)keys_by_op})
-    if (p) cudaFreeAsync(p, s);
-  return rc;
+  if (ops)  // split by op byte; each upsert segment is combined (run_device_by_kind)
+    return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, cx);
+  if (vout) WS_CK(cudaMemsetAsync(vout, 0, 8 * n, s));
+  return combine_uniform(t, uop, keys, vals, n, status, s, flags, cx);
 }
 
 // Host-buffer batches: staged through device memory in 4M-op chunks on three
