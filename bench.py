@@ -227,6 +227,40 @@ def cpu_port_rate(n_slots: int, load: float, threads: int, seed: int = 42):
                                  f"50/50 queries per shard ({ops} ops)")
 
 
+def reference_cpython_rate(load: float, threads: int, log2_slots: int = 18, seed: int = 42):
+    """The UNMODIFIED reference package (warpbench, installed into
+    baseline/_ref from /root/reference with pip --target) through its own
+    public API and timed runners: make_table(TableConfig(p2_md)) then
+    bench/runners.py:130-144 timed_insert / timed_query on `threads` threads
+    (GIL-bound pure Python).  Returns a dict, or {"unavailable": why}."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "warpbench")):
+        return {"unavailable": "baseline/_ref/warpbench not installed (see DESIGN.md section 6)"}
+    if ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        from warpbench.bench.keys import gen_uniform_keys as rkeys
+        from warpbench.bench.runners import timed_insert, timed_query
+        from warpbench.core import TableConfig as RCfg
+        from warpbench.tables import make_table as rmake
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"reference import failed: {exc!r}"}
+    slots = 1 << log2_slots
+    n = int(slots * load)
+    t = rmake(RCfg(design="p2_md", capacity_slots=slots, seed=seed))
+    keys = [int(x) for x in rkeys(seed, n)]
+    miss = [int(x) for x in rkeys(seed + 1, n - n // 2)]
+    dt_i, full = timed_insert(t, keys, threads)
+    dt_h, m1 = timed_query(t, keys[: n // 2], threads, expect_found=True)
+    dt_m, m2 = timed_query(t, miss, threads, expect_found=False)
+    dt = dt_i + dt_h + dt_m
+    return {"value": round(2 * n / dt / 1e6, 4), "unit": UNIT, "threads": threads,
+            "insert_mops": round(n / dt_i / 1e6, 4), "query_mops": round(n / (dt_h + dt_m) / 1e6, 4),
+            "seconds": round(dt, 2), "full": full, "query_mismatches": m1 + m2,
+            "sample": f"reference warpbench P2MdTable 2^{log2_slots} slots: {n} inserts + {n} 50/50 queries "
+                      "(bench/runners.py timed_insert / timed_query)"}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -255,6 +289,8 @@ def run_reference(args, rank, world):
                    "load": args.load},
         "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": desc},
+        # the reference itself (pure Python), BASELINE.md section 3
+        "reference_cpython": [reference_cpython_rate(args.load, th) for th in sorted({1, threads})],
         "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -435,7 +471,8 @@ def run_ours(args, rank, world):
         threads = 1
         r, dt, desc = cpu_port_rate(1 << 22, args.load, threads)
         cpu = {"value": round(r, 3), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": desc + f"; {dt:.2f} s"}
+               "sample": desc + f"; {dt:.2f} s",
+               "reference_cpython": reference_cpython_rate(args.load, 1)}
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),

@@ -856,6 +856,7 @@ struct Ctx {
     const int n = B();
     u64 uq[8];
     const int nu = ck_buckets(key, uq);
+    bool final_scan = false;  // a resumed op that found no path rescans its own buckets once
     for (int attempt = 0; attempt < CUCKOO_RETRIES; attempt++) {
       if (attempt > 0 || !d.ck_resume) {
         ck_lock_all(uq, nu);
@@ -875,6 +876,7 @@ struct Ctx {
         ck_unlock_all(uq, nu);
         if (st != 0xFF) return st;
         if (free_at >= 0) continue;  // lost a race for the free cell: retry
+        if (final_scan) return S_FULL;
       }
       if (d.depth >= 1) {
         u64 mv1[4];
@@ -890,7 +892,12 @@ struct Ctx {
       bool ok = false;
       if (len > 0) ok = ck_execute(ws + 4 * (d.bfs_entries - (u64)len), len);
       ws_release(wid);
-      if (len < 0) return S_FULL;
+      if (len < 0) {
+        // a resumed op skipped the locked scan of attempt 0; its buckets may
+        // have gained the key or a free cell during the eviction launch
+        if (attempt == 0 && d.ck_resume) { final_scan = true; continue; }
+        return S_FULL;
+      }
       (void)ok;  // a failed move means the world changed: retry the insert
     }
     return S_FULL;
