@@ -186,6 +186,61 @@ void run(const char* buf, u64 bytes, u64* out, int blocks, int iters, const char
   printf("%-28s W=%4d R=%d  %8.2f G acc/s  %8.1f GB/s useful\n", name, W, R, acc / ms / 1e6, acc * W / ms / 1e6);
 }
 
+// query-shaped dependent chains: a random 32 B tag-block read in T (1/8 of
+// the footprint, as the tag array is to the cells) and then a dependent random
+// 16 B cell read in C, R chains per thread.  Mode 'q' runs it over the whole
+// buffer split 1:8 (powers of two), so 4608 MiB ~ the 2^28-slot table, 18432 MiB ~ 2^30:
+// does the rate fall with the footprint (TLB reach) as the query's does?
+template <int R>
+__global__ void __launch_bounds__(256) chain(const char* tags, u64 ntag, const char* cells, u64 ncell, u64 seed,
+                                             u64* out, int iters) {
+  u64 acc = 0;
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; it++) {
+    u64 h[R], a[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      h[r] = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40));
+      u64 x, y, z, w;
+      ld32<3>(tags + (h[r] & (ntag - 1)) * 64, x, y, z, w);
+      a[r] = x ^ y ^ z ^ w;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      u64 x, y;
+      ld16<3>(cells + (((h[r] >> 20) ^ (a[r] & 1)) & (ncell - 1)) * 16, x, y);
+      acc ^= x ^ y;
+    }
+  }
+  if (acc == 0x123456789ull) out[0] = acc;
+}
+
+// the same chains over a bucket-interleaved layout: bucket b = 64 B of tags
+// then 512 B of cells at b * 576, so a bucket's tag block and its cells share
+// one 2 MiB page (one TLB entry per chain instead of two)
+template <int R>
+__global__ void __launch_bounds__(256) chain_colo(const char* buf, u64 nb, u64 seed, u64* out, int iters) {
+  u64 acc = 0;
+  const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+  for (int it = 0; it < iters; it++) {
+    u64 h[R], a[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      h[r] = mix64(seed ^ (tid * R + r) ^ ((u64)it << 40));
+      u64 x, y, z, w;
+      ld32<3>(buf + (h[r] & (nb - 1)) * 576, x, y, z, w);
+      a[r] = x ^ y ^ z ^ w;
+    }
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      u64 x, y;
+      ld16<3>(buf + (h[r] & (nb - 1)) * 576 + 64 + (((h[r] >> 40) ^ (a[r] & 1)) & 31) * 16, x, y);
+      acc ^= x ^ y;
+    }
+  }
+  if (acc == 0x123456789ull) out[0] = acc;
+}
+
 int main(int argc, char** argv) {
   const u64 mb = argc > 1 ? strtoull(argv[1], 0, 10) : 4096;  // a power of two (index masks)
   const u64 bytes = mb << 20;
@@ -211,6 +266,40 @@ int main(int argc, char** argv) {
       run_coop<2, 16>(buf, bytes, out, bl, iters, "coop 2 lanes (1 instr)");
       run_coop<4, 8>(buf, bytes, out, bl, iters, "coop 4 lanes (1 instr)");
       run_coop<4, 16>(buf, bytes, out, bl, iters, "coop 4 lanes (1 instr)");
+    }
+    cudaDeviceSynchronize();
+    return 0;
+  }
+  if (argc > 2 && argv[2][0] == 'q') {
+    const u64 tb = bytes / 9 & ~63ull, ntag = 1ull << (63 - __builtin_clzll(tb / 64));
+    const char* cells = buf + ntag * 64;
+    const u64 ncell = 1ull << (63 - __builtin_clzll((bytes - ntag * 64) / 16));
+    for (int bps : {4, 8}) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a); cudaEventCreate(&b);
+      chain<2><<<148 * bps, 256>>>(buf, ntag, cells, ncell, 1, out, 1);
+      cudaEventRecord(a);
+      chain<2><<<148 * bps, 256>>>(buf, ntag, cells, ncell, 7, out, iters);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      const double ch = (double)148 * bps * 256 * 2 * iters;
+      printf("chain tags %6llu MiB + cells %6llu MiB, %d CTAs/SM: %6.2f G chains/s = %6.2f G acc/s\n",
+             ntag * 64 >> 20, ncell * 16 >> 20, bps, ch / ms / 1e6, 2 * ch / ms / 1e6);
+    }
+    const u64 nb = 1ull << (63 - __builtin_clzll(bytes / 576));
+    for (int bps : {4, 8}) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a); cudaEventCreate(&b);
+      chain_colo<2><<<148 * bps, 256>>>(buf, nb, 1, out, 1);
+      cudaEventRecord(a);
+      chain_colo<2><<<148 * bps, 256>>>(buf, nb, 7, out, iters);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b);
+      const double ch = (double)148 * bps * 256 * 2 * iters;
+      printf("colocated %8llu buckets x 576 B = %6llu MiB, %d CTAs/SM: %6.2f G chains/s = %6.2f G acc/s\n",
+             nb, nb * 576 >> 20, bps, ch / ms / 1e6, 2 * ch / ms / 1e6);
     }
     cudaDeviceSynchronize();
     return 0;
