@@ -20,10 +20,15 @@ schema CSV rows (instrument.Row).
 
 from __future__ import annotations
 
+import contextlib
+import json
+import os
+import time
+
 import numpy as np
 
 from .core import TableConfig
-from .instrument import Row
+from .instrument import Row, write_csv
 from .workload import derive_seed, gen_uniform_keys, kmer_keys, mix64_np, zipf_ranks
 
 U64 = np.uint64
@@ -71,6 +76,76 @@ def _mops(n, ms):
     return n / ms / 1e3 if ms > 0 else 0.0
 
 
+# ------------------------------------------------------------ CSV + manifest
+
+def manifest_lines(benchmark: str, table, seed: int, extra=()) -> list:
+    """The reference's '#'-prefixed CSV manifest (bench/runners.py:66-86),
+    field for field; `threads` is 0 (one device launch per batch, no host
+    thread pool) and `slot_engine` / `wide_atomic` come from the table's
+    capability report."""
+    from . import __version__
+    cfg = table.config
+    cap = table.capability_report()
+    lines = [
+        f"benchmark={benchmark}",
+        f"design={cfg.design}",
+        f"capacity_slots={table.capacity_slots}",
+        f"bucket_size={table.bucket_size}",
+        f"line_bytes={cfg.line_bytes}",
+        f"probe_cap={cfg.probe_cap}",
+        f"mode={cfg.mode}",
+        f"seed={seed}",
+        "threads=0",
+        f"slot_engine={cap['slot_engine']}",
+        f"wide_atomic={cap['wide_atomic']}",
+        f"num_buckets={table.num_buckets}",
+        f"version={__version__}",
+        f"timestamp={time.strftime('%Y-%m-%dT%H:%M:%S')}",
+    ]
+    lines.extend(extra)
+    return lines
+
+
+def write_report_csv(out_dir, benchmark: str, table, rows, seed: int, extra=()) -> str:
+    """`{out_dir}/{benchmark}_{design}.csv` in the reference schema
+    (instrument.CSV_HEADER) with the manifest above; returns the path."""
+    path = os.path.join(out_dir, f"{benchmark}_{table.config.design}.csv")
+    write_csv(path, manifest_lines(benchmark, table, seed, extra), rows)
+    return path
+
+
+# ------------------------------------------------------- ncu range markers
+# WS_NCU_RANGES=<file>: every timed batch of the runners becomes one
+# cudaProfilerStart/Stop range opened by a one-element torch fill (the range
+# marker), and the range's (design, op, load) label is appended to <file>.
+# Under `ncu --profile-from-start off` the launch list is then the marker,
+# the batch's kernels, the next marker, ... -- scripts/ncu_ranges.py joins
+# it with the labels into DRAM sectors per op for every load point.
+_NCU_MARK = None
+
+
+@contextlib.contextmanager
+def _ncu_range(label: dict, ops: int):
+    path = os.environ.get("WS_NCU_RANGES")
+    if not path:
+        yield
+        return
+    global _NCU_MARK
+    torch = _torch()
+    if _NCU_MARK is None:
+        _NCU_MARK = torch.zeros(1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    _NCU_MARK.fill_(1)
+    try:
+        yield
+    finally:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        with open(path, "a", encoding="utf-8") as fh:
+            fh.write(json.dumps({**label, "ops": int(ops)}) + "\n")
+
+
 def run_config1(seed: int = 42, capacity: int = 1 << 20, design: str = "double") -> dict:
     from .tables import make_table
     t = make_table(TableConfig(design=design, capacity_slots=capacity, seed=seed))
@@ -102,7 +177,7 @@ def run_config1(seed: int = 42, capacity: int = 1 << 20, design: str = "double")
 
 def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_POINTS,
                    query_sample: int = 1 << 20, probe_sample: int = 4096, mode: str = "concurrent",
-                   drain: bool = True) -> dict:
+                   drain: bool = True, out_dir: str | None = None) -> dict:
     """Insert to each load point (timed batch), 50/50 queries (timed), probe
     means from instrumented batches (reference ProbeRecorder semantics), then
     an erase drain in 18 slices."""
@@ -131,7 +206,7 @@ def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_
         np_ins = min(probe_sample, len(batch) // 4)
         timed = batch[: len(batch) - np_ins]
         d_timed = _dev(timed, dev)  # H2D outside the timed region
-        with _Timer() as ti:
+        with _ncu_range({"design": design, "op": "insert", "load": point}, len(timed)), _Timer() as ti:
             st = t.upsert_batch(d_timed, d_timed, check=False)
         st_np = _np(st)
         fulls += int((st_np == 2).sum())
@@ -150,7 +225,7 @@ def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_
         pos = live_keys[np.linspace(0, len(live_keys) - 1, qn // 2).astype(np.int64)]
         q = np.concatenate([pos, neg[: qn - len(pos)]])
         d_q = _dev(q, dev)
-        with _Timer() as tq:
+        with _ncu_range({"design": design, "op": "query_5050", "load": point}, qn), _Timer() as tq:
             found, _vals = t.query_batch(d_q, check=False)
         f = _np(found).astype(bool)
         ok = bool(f[: len(pos)].all() and not f[len(pos):].any())
@@ -174,14 +249,16 @@ def run_load_sweep(design: str, capacity: int, seed: int = 42, load_points=LOAD_
         for off in range(0, len(live), chunk):
             sl = live[off:off + chunk]
             d_sl = _dev(sl, dev)
-            with _Timer() as te:
+            with _ncu_range({"design": design, "op": "erase", "load": round((len(live) - off) / cap, 4)},
+                            len(sl)), _Timer() as te:
                 gone = t.erase_batch(d_sl, check=False)
             rows.append(Row(design, mode, cap, 128, "throughput", "erase", round((len(live) - off) / cap, 4), 0,
                             len(sl), te.ms / 1e3, _mops(len(sl), te.ms)))
             if not bool(_np(gone).all()):
                 points.append({"drain_error": off})
         points.append({"after_drain_occupied": t.occupied_count()})
-    return {"design": design, "capacity": cap, "fulls": fulls, "points": points, "rows": rows}
+    csv = write_report_csv(out_dir, "load", t, rows, seed, [f"fulls={fulls}"]) if out_dir else None
+    return {"design": design, "capacity": cap, "fulls": fulls, "points": points, "rows": rows, "csv": csv}
 
 
 def run_aging(design: str = "iceberg_md", capacity: int = 1 << 26, iterations: int = 20,
@@ -284,7 +361,8 @@ def _probe_means(t, ops, keys, vals, kinds, serial=False):
 
 
 def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_fraction: float = 0.01,
-                      seed: int = 42, probe_sample: int = 200, line_bytes: int = 128) -> dict:
+                      seed: int = 42, probe_sample: int = 200, line_bytes: int = 128,
+                      out_dir: str | None = None) -> dict:
     """The reference's aging workload restated (bench/runners.py:259-353):
     fill to 85%, then per iteration one concurrent mixed launch that inserts
     a 1% slice of new keys (value k & 0xFFFF), erases the oldest 1%, queries
@@ -318,8 +396,10 @@ def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_f
         kinds, keys = kinds[order], keys[order]
         ops = np.where(kinds == 0, OP_UPSERT, np.where(kinds == 1, OP_ERASE, OP_QUERY)).astype(np.uint8)
         vals = np.where(kinds == 0, keys & U64(0xFFFF), U64(0))
-        with _Timer() as tm:
-            s, _v = t.mixed_batch(_dev(ops, dev), _dev(keys, dev), _dev(vals, dev), check=False)
+        d_ops, d_keys, d_vals = _dev(ops, dev), _dev(keys, dev), _dev(vals, dev)
+        with _ncu_range({"design": design, "op": "mixed", "load": round(fill_n / cap, 4), "iteration": it},
+                        len(ops)), _Timer() as tm:
+            s, _v = t.mixed_batch(d_ops, d_keys, d_vals, check=False)
         s = _np(s)
         ok = bool((s[kinds == 0] == 0).all() and (s[kinds == 1] == 1).all() and
                   (s[kinds == 2] == 1).all() and not s[kinds == 3].any())
@@ -341,12 +421,14 @@ def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_f
         for kind, m in means.items():
             rows.append(Row(design, "concurrent", cap, line_bytes, "probe", kind, lf, 1, probe_n, 0.0, 0.0, m))
         its.append({"iteration": it, "probe_means": means, "mops": _mops(len(ops), tm.ms), "ok": ok})
+    csv = write_report_csv(out_dir, "aging", t, rows, seed) if out_dir else None
     return {"design": design, "capacity": cap, "slice": slice_n, "iterations": its, "ok": ok_all,
-            "occupied": t.occupied_count(), "fill_n": fill_n, "rows": rows}
+            "occupied": t.occupied_count(), "fill_n": fill_n, "rows": rows, "csv": csv}
 
 
 def run_scaling(design: str, sizes=(1 << 17, 1 << 20, 1 << 23), seed: int = 42, probe_sample: int = 4096,
-                query_sample: int = 1 << 20, line_bytes: int = 128, probe_window: float = 0.0) -> dict:
+                query_sample: int = 1 << 20, line_bytes: int = 128, probe_window: float = 0.0,
+                out_dir: str | None = None) -> dict:
     """Insert to 90% and positive-query throughput plus probe means per table
     size (reference bench/runners.py:356-405): the last stretch of the fill
     is inserted instrumented, then instrumented positive / negative queries.
@@ -364,14 +446,16 @@ def run_scaling(design: str, sizes=(1 << 17, 1 << 20, 1 << 23), seed: int = 42, 
                        else min(probe_sample, max(1, fill_n // 5)))
         n = fill_n - probe_ins_n
         keys = gen_uniform_keys(derive_seed(seed, size), fill_n)
-        dk = _dev(keys[:n], dev)
-        with _Timer() as ti:
-            st = t.upsert_batch(dk, _dev(keys[:n] & U64(0xFFFF), dev), check=False)
+        dk, dv = _dev(keys[:n], dev), _dev(keys[:n] & U64(0xFFFF), dev)  # H2D outside the timed region
+        with _ncu_range({"design": design, "op": "insert", "load": 0.9, "size": cap}, n), _Timer() as ti:
+            st = t.upsert_batch(dk, dv, check=False)
         fulls = int((_np(st) == 2).sum())
         stride = max(1, n // min(query_sample, n))
         pos = keys[:n][::stride][:min(query_sample, n)]
-        with _Timer() as tq:
-            f, _v = t.query_batch(_dev(pos, dev), check=False)
+        d_pos = _dev(pos, dev)
+        with _ncu_range({"design": design, "op": "query_pos", "load": 0.9, "size": cap}, len(pos)), \
+                _Timer() as tq:
+            f, _v = t.query_batch(d_pos, check=False)
         miss = int((~_np(f).astype(bool)).sum())
         ins_ops = np.full(probe_ins_n, OP_UPSERT, np.uint8)
         pst, _pv, m_ins = _probe_means(t, ins_ops, keys[n:], np.ones(probe_ins_n, U64),
@@ -393,8 +477,9 @@ def run_scaling(design: str, sizes=(1 << 17, 1 << 20, 1 << 23), seed: int = 42, 
             rows.append(Row(design, "concurrent", cap, line_bytes, "probe", kind, 0.9, 1, 0, 0.0, 0.0, m))
         per_size.append({"size": cap, "probe_means": means, "fulls": fulls, "missing": miss,
                          "insert_mops": _mops(n, ti.ms), "query_mops": _mops(len(pos), tq.ms)})
-        del t
-    return {"design": design, "per_size": per_size, "rows": rows}
+        last = t
+    csv = write_report_csv(out_dir, "scaling", last, rows, seed) if out_dir and sizes else None
+    return {"design": design, "per_size": per_size, "rows": rows, "csv": csv}
 
 
 def run_kmer(genome_len: int = 1 << 24, k: int = 31, capacity: int = 1 << 25, design: str = "p2_md",
