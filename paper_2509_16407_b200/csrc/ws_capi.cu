@@ -206,6 +206,18 @@ u64* pin() {
   return tp.p;
 }
 
+// a second pinned block of the calling thread (512 words) for the bin starts
+// of run_device_split, which outlive nested calls that use pin()
+u64* pin_call() {
+  struct Pin {
+    u64* p = nullptr;
+    ~Pin() { if (p) cudaFreeHost(p); }
+  };
+  thread_local Pin tp;
+  if (!tp.p && cudaMallocHost((void**)&tp.p, 512 * 8) != cudaSuccess) tp.p = nullptr;
+  return tp.p;
+}
+
 // H2D / D2H staging streams and events of the calling thread on one device
 struct Staging {
   cudaStream_t s_in = nullptr, s_aux = nullptr;
@@ -361,12 +373,203 @@ __global__ void k_seg_starts(const u8* __restrict__ op_sorted, u64 n, u64* start
 // stream, then the results are scattered back.  Running the segments in
 // sequence is one serial order of the concurrent batch.
 int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status, cudaStream_t s,
-                    u32 flags, const CallCtx& cx);
+                    u32 flags, const CallCtx& cx, const u32* oidx, const u64* dn, u64 nbatch);
+
+// ---- split by kind without a sort or a blocking read-back
+// A counting partition by op byte (one histogram pass, a scan of the
+// bin-major [256 x blocks] counts, one scatter pass; order within a bin is
+// arbitrary, so every op carries its batch index) writes the erases and the
+// queries into regions of their own, whose bases the host knows, and every
+// other op byte into a third region ordered by op byte.  The erase and query
+// segments are launched at once with their device-resident counts; the host
+// waits only for the 257 bin starts (an event behind the partition) while
+// the GPU runs them, then launches the upsert segments at known offsets.
+constexpr int kKindTile = 256;
+
+// per-block chunk, a multiple of 32 so every warp's lanes share one loop bound
+__device__ __forceinline__ u32 kind_chunk(u64 n, u32 nblk) { return (u32)(((n + nblk - 1) / nblk + 31) & ~31ull); }
+
+__global__ void __launch_bounds__(kKindTile) k_kind_hist(const u8* __restrict__ ops, u64 n, u32* H) {
+  __shared__ u32 h[256];
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+  __syncthreads();
+  const u32 ch = kind_chunk(n, gridDim.x);
+  const u64 lo = (u64)blockIdx.x * ch, hi = lo + ch < n ? lo + ch : n;
+  for (u64 i = lo + threadIdx.x; i < ((hi + 31) & ~31ull) && lo < hi; i += blockDim.x) {
+    const bool act = i < hi;
+    const u32 b = act ? ops[i] : 256u;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, b);
+    if (act && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[b], (u32)__popc(peers));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) H[(u64)b * gridDim.x + blockIdx.x] = h[b];
+}
+
+struct KindOut {
+  u64 *ke, *kq, *kr, *vr;
+  u32 *ie, *iq, *ir;
+  u8* opr;
+};
+
+// S: exclusive scan of H (bin-major).  Bin 1 (erase) and bin 2 (query) go to
+// their own regions; every other bin to the rest region, shifted down by the
+// erase and query counts when it sorts above them.
+__global__ void __launch_bounds__(kKindTile) k_kind_split(const u8* __restrict__ ops, const u64* __restrict__ keys,
+                                                          const u64* __restrict__ vals, u64 n, const u32* S,
+                                                          KindOut o) {
+  __shared__ u32 cur[256];
+  const u32 nb = gridDim.x;
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) cur[b] = S[(u64)b * nb + blockIdx.x];
+  const u32 s1 = S[1ull * nb], s2 = S[2ull * nb], s3 = S[3ull * nb];
+  __syncthreads();
+  const u32 ch = kind_chunk(n, nb);
+  const u64 lo = (u64)blockIdx.x * ch, hi = lo + ch < n ? lo + ch : n;
+  for (u64 i = lo + threadIdx.x; i < ((hi + 31) & ~31ull) && lo < hi; i += blockDim.x) {
+    const bool act = i < hi;
+    const u32 b = act ? ops[i] : 256u;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, b);
+    const int lane = threadIdx.x & 31, first = __ffs(peers) - 1;
+    u32 base = 0;
+    if (act && lane == first) base = atomicAdd(&cur[b], (u32)__popc(peers));
+    base = __shfl_sync(0xFFFFFFFFu, base, first);
+    if (!act) continue;
+    const u32 p = base + __popc(peers & ((1u << lane) - 1));
+    const u64 k = keys[i];
+    if (b == 1) {
+      o.ke[p - s1] = k;
+      o.ie[p - s1] = (u32)i;
+    } else if (b == 2) {
+      o.kq[p - s2] = k;
+      o.iq[p - s2] = (u32)i;
+    } else {
+      const u32 r = b > 2 ? p - (s3 - s1) : p;
+      o.kr[r] = k;
+      o.vr[r] = vals[i];
+      o.ir[r] = (u32)i;
+      o.opr[r] = (u8)b;
+    }
+  }
+}
+
+// bin starts S[b][0] (b = 0..255) and n, plus the erase / query / rest counts
+__global__ void k_kind_starts(const u32* S, u32 nb, u64 n, u64* starts, u64* cnt) {
+  const int b = threadIdx.x;
+  starts[b] = S[(u64)b * nb];
+  if (b == 0) {
+    starts[256] = n;
+    const u64 s1 = S[1ull * nb], s2 = S[2ull * nb], s3 = S[3ull * nb];
+    cnt[0] = s2 - s1;
+    cnt[1] = s3 - s2;
+    cnt[2] = n - (s3 - s1);
+  }
+}
+
+// results back to batch order; region 0 erases, 1 queries, 2 the rest
+__global__ void k_kind_unsplit(const u64* cnt, const u32* ie, const u8* ste, const u32* iq, const u8* stq,
+                               const u64* voq, const u32* ir, const u8* str, const u64* vor, const u8* opr,
+                               u8* status, u64* vout) {
+  const int g = blockIdx.y;
+  const u64 m = cnt[g];
+  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < m; j += (u64)gridDim.x * blockDim.x) {
+    if (g == 0) {
+      const u32 i = ie[j];
+      if (status) status[i] = ste[j];
+      if (vout) vout[i] = 0;
+    } else if (g == 1) {
+      const u32 i = iq[j];
+      if (status) status[i] = stq[j];
+      if (vout) vout[i] = voq[j];
+    } else {
+      const u32 i = ir[j];
+      if (status) status[i] = str[j];
+      if (vout) vout[i] = (opr[j] & 15) == OP_QUERY ? vor[j] : 0;
+    }
+  }
+}
+
+int run_device_split(ws_table* t, const u8* ops, const u64* keys, const u64* vals, u64 n, u8* status, u64* vout,
+                     cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, const CallCtx& cx) {
+  const u32 nblk = (u32)std::max<u64>(1, std::min<u64>((u64)kSMs * 8, (n + 2047) / 2048));
+  const u64 nh = 256ull * nblk;
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, (u32*)nullptr, (u32*)nullptr, (int64_t)nh, s);
+  // one scratch allocation, carved
+  const u64 need = n * (8 + 4 + 1) + n * (8 + 4 + 1 + 8) + n * (8 + 8 + 4 + 1 + 1 + 8) + 8 * nh + 257 * 8 + 3 * 8 +
+                   tb + 24 * 128;
+  char* buf = nullptr;
+  WS_CK(cudaMallocAsync((void**)&buf, need, s));
+  char* p = buf;
+  auto carve = [&](u64 bytes) { char* r = p; p += (bytes + 127) & ~127ull; return (void*)r; };
+  KindOut o;
+  o.ke = (u64*)carve(8 * n); o.ie = (u32*)carve(4 * n); u8* ste = (u8*)carve(n);
+  o.kq = (u64*)carve(8 * n); o.iq = (u32*)carve(4 * n); u8* stq = (u8*)carve(n); u64* voq = (u64*)carve(8 * n);
+  o.kr = (u64*)carve(8 * n); o.vr = (u64*)carve(8 * n); o.ir = (u32*)carve(4 * n); o.opr = (u8*)carve(n);
+  u8* str = (u8*)carve(n); u64* vor = (u64*)carve(8 * n);
+  u32* H = (u32*)carve(4 * nh); u32* S = (u32*)carve(4 * nh);
+  u64* starts = (u64*)carve(257 * 8); u64* cnt = (u64*)carve(3 * 8);
+  void* tmp = carve(tb + 16);
+  const u32 inner = (flags & ~(WS_F_SYNC_CHECK | WS_F_COMBINE)) | kF_NO_KIND_SORT |
+                    ((flags & WS_F_NO_CHECK) ? 0u : (kF_VALIDATED | WS_F_NO_CHECK));
+  const bool comb = (flags & WS_F_COMBINE) != 0;
+  k_kind_hist<<<nblk, kKindTile, 0, s>>>(ops, n, H);
+  cub::DeviceScan::ExclusiveSum(tmp, tb, H, S, (int64_t)nh, s);
+  k_kind_split<<<nblk, kKindTile, 0, s>>>(ops, keys, vals, n, S, o);
+  k_kind_starts<<<1, 256, 0, s>>>(S, nblk, n, starts, cnt);
+  int rc = cuda_err(cudaGetLastError());
+  u64* hst = pin_call();
+  if (!hst) rc = WS_ERR_ALLOC;
+  cudaEvent_t ev = nullptr;
+  if (!rc) rc = cuda_err(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  if (!rc) rc = cuda_err(cudaMemcpyAsync(hst, starts, 257 * 8, cudaMemcpyDeviceToHost, s));
+  if (!rc) rc = cuda_err(cudaEventRecord(ev, s));
+  // erases and queries at once, their counts read on the device
+  if (!rc) {
+    CallCtx ce = cx;
+    ce.dn = cnt;
+    rc = run_device_plain(t, nullptr, OP_ERASE, o.ke, nullptr, n, ste, nullptr, s, inner, true, false, false, ce);
+  }
+  if (!rc) {
+    CallCtx cq = cx;
+    cq.dn = cnt + 1;
+    rc = run_device_plain(t, nullptr, OP_QUERY, o.kq, nullptr, n, stq, voq, s, inner, false, false, true, cq);
+  }
+  if (!rc) rc = cuda_err(cudaEventSynchronize(ev));
+  std::vector<u64> st_h(257, 0);
+  if (!rc) std::copy(hst, hst + 257, st_h.begin());
+  const u64* hs = st_h.data();
+  // the rest region, one segment per op byte present, in op-byte order
+  const u64 c1 = hs[2] - hs[1], c2 = hs[3] - hs[2];
+  for (int v = 0; v < 256 && !rc; v++) {
+    if (v == 1 || v == 2) continue;
+    const u64 lo = hs[v] - (v > 2 ? c1 + c2 : 0), m = hs[v + 1] - hs[v];
+    if (!m) continue;
+    const int kind = v & 15, merge = v >> 4;
+    if (kind == OP_UPSERT && merge <= M_MIN) {
+      rc = comb && m >= 2 ? combine_uniform(t, (u8)v, o.kr + lo, o.vr + lo, m, str + lo, s, inner, cx, o.ir + lo,
+                                            nullptr, n)
+                          : run_device_plain(t, nullptr, (u8)v, o.kr + lo, o.vr + lo, m, str + lo, nullptr, s, inner,
+                                             false, true, false, cx);
+    } else {  // erase / query bytes with stray merge bits, invalid bytes (gated): the generic kernel
+      rc = run_device_plain(t, o.opr + lo, 0, o.kr + lo, o.vr + lo, m, str + lo, vor + lo, s, inner, has_erase,
+                            has_upsert, false, cx);
+    }
+  }
+  if (!rc) {
+    dim3 g(grid_for(n), 3);
+    k_kind_unsplit<<<g, kThreads, 0, s>>>(cnt, o.ie, ste, o.iq, stq, voq, o.ir, str, vor, o.opr, status, vout);
+    rc = cuda_err(cudaGetLastError());
+  }
+  if (ev) cudaEventDestroy(ev);
+  cudaFreeAsync(buf, s);
+  return rc;
+}
 
 int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status,
                        u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert, const CallCtx& cx) {
   int rc = validate(keys, ops, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
   if (rc) return rc;
+  if (vals && n < (1ull << 31)) return run_device_split(t, ops, keys, vals, n, status, vout, s, flags, has_erase,
+                                                          has_upsert, cx);
   u8 *op_p = nullptr, *st_p = nullptr;
   u32 *idx = nullptr, *perm = nullptr;
   u64 *k_p = nullptr, *v_p = nullptr, *vo_p = nullptr, *starts = nullptr;
@@ -405,7 +608,7 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
     const int kind = v & 15, merge = v >> 4;
     const u64 m = hi - lo;
     if (kind == OP_UPSERT && merge <= M_MIN && v_p) {
-      rc = comb && m >= 2 ? combine_uniform(t, v, k_p + lo, v_p + lo, m, st_p + lo, s, inner, cx)
+      rc = comb && m >= 2 ? combine_uniform(t, v, k_p + lo, v_p + lo, m, st_p + lo, s, inner, cx, nullptr, nullptr, 0)
                           : run_device_plain(t, nullptr, v, k_p + lo, v_p + lo, m, st_p + lo, nullptr, s, inner,
                                              false, true, false, cx);
       if (vo_p && !rc) rc = cuda_err(cudaMemsetAsync(vo_p + lo, 0, 8 * m, s));
@@ -495,86 +698,66 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
 // the table; one op per (key, merge) group is applied and the statuses are
 // expanded: the group leader gets the real status, the other members
 // UPDATED (FULL if the leader was).  Equivalent to a serial order of the
-// batch in which each group's upserts run back to back; the point is Zipf
-// hot keys, whose ops would otherwise serialise on one bucket lock.
+// batch in which each group's upserts run back to back, in batch-index order;
+// the point is Zipf hot keys, whose ops would otherwise serialise on one
+// bucket lock.
 //   * mixed batches are first split by op byte (run_device_by_kind); every
 //     upsert segment (one merge) is then combined on its own;
-//   * commutative merges (ADD / MAX / MIN): hash aggregation into an
-//     L2-resident open-addressing table (claim by CAS, fold by one atomic
-//     per op), compaction of the occupied slots, apply with the group count
-//     read on the device -- no sort and no host synchronisation;
-//   * REPLACE / KEEP: a stable 64-bit key sort keeps batch-index order inside
-//     each key's run, so the fold reproduces the index order (last REPLACE /
-//     first KEEP wins, as the sequential reference would).
-struct OpVal {
-  u64 v;
-  u32 op;
-  u32 pad;
-};
-struct CombineOp {
-  __device__ __forceinline__ OpVal operator()(const OpVal& a, const OpVal& b) const {
-    const int m = a.op >> 4;
-    OpVal r = a;
-    r.v = m == M_KEEP ? a.v : apply_merge(m, a.v, b.v);
-    return r;
-  }
-};
-
+//   * every merge uses hash aggregation into an L2-resident open-addressing
+//     table (claim by CAS): ADD / MAX / MIN fold the values with one atomic
+//     per warp group; REPLACE keeps the value of the group's HIGHEST batch
+//     index (atomicMax on index+1: the last write of the serial order), KEEP
+//     the value of its LOWEST (the first write; later KEEPs keep it).  The
+//     leader -- the op reporting INSERTED for a new key -- is the lowest batch
+//     index.  Compaction of the leaders, then the apply, with the group count
+//     read on the device: no sort and no host synchronisation.
+//   * `oidx` (optional) maps a segment position to its batch index when the
+//     segment was gathered out of order (run_device_by_kind); `dn` (optional)
+//     is the segment's device-resident length (n = its upper bound).
 __global__ void k_comb_iota(u64 n, u32* idx) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) idx[i] = (u32)i;
 }
 
-__global__ void k_comb_heads(const u64* sk, const u32* si, u8 uop, const u64* vals, u64 n, u32* head, OpVal* ov) {
-  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
-    head[j] = j == 0 || sk[j] != sk[j - 1];
-    ov[j] = OpVal{vals ? vals[si[j]] : 0ull, uop, 0};
-  }
-}
-
-__global__ void k_comb_groups(const u64* sk, const u32* head, const u32* seg, u64 n, u64* gkey) {
-  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x)
-    if (head[j]) gkey[seg[j] - 1] = sk[j];
-}
-
-__global__ void k_comb_vals(const OpVal* agg, const u64* ng, u64 n, u64* gval) {
-  const u64 m = *ng < n ? *ng : n;
-  for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < m; g += (u64)gridDim.x * blockDim.x)
-    gval[g] = agg[g].v;
-}
-
-__global__ void k_comb_expand(const u32* si, const u32* head, const u32* seg, u64 n, const u8* gst, u8* status) {
-  for (u64 j = blockIdx.x * (u64)blockDim.x + threadIdx.x; j < n; j += (u64)gridDim.x * blockDim.x) {
-    const u8 gs = gst[seg[j] - 1];
-    status[si[j]] = head[j] ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
-  }
-}
-
-// hash aggregation of one commutative-merge upsert batch.  Lanes of a warp
-// holding the same key fold their values first (__match_any_sync), so a Zipf
-// hot key costs one table atomic per warp instead of one per op.
 __device__ __forceinline__ u64 merge_of(int merge, u64 a, u64 b) {
   return merge == M_ADD ? a + b : merge == M_MAX ? (a > b ? a : b) : (a < b ? a : b);
 }
+__device__ __forceinline__ u64 dev_n(u64 n, const u64* dn) { return dn && *dn < n ? *dn : n; }
+
+// Lanes of a warp holding the same key fold first (__match_any_sync), so a
+// Zipf hot key costs one table atomic per warp instead of one per op.
 __global__ void __launch_bounds__(256) k_agg_insert(const u64* __restrict__ keys, const u64* __restrict__ vals,
-                                                    u64 n, int merge, u64* tk, u64* tv, u32* leader, u64 mask,
-                                                    u32* grp) {
+                                                    const u32* __restrict__ oidx, u64 n, const u64* dn, int merge,
+                                                    u64* tk, u64* tv, u32* leader, u64 mask, u32* grp) {
+  n = dev_n(n, dn);
   const int lane = threadIdx.x & 31;
+  const bool fold = merge == M_ADD || merge == M_MAX || merge == M_MIN;
   for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n;
        base += (u64)gridDim.x * blockDim.x) {
     const u64 i = base + lane;
     const bool act = i < n;
     const u64 key = act ? __ldg(keys + i) : 0ull;
-    u64 v = act ? __ldg(vals + i) : 0ull;
+    const u64 v0 = act && fold ? __ldg(vals + i) : 0ull;
+    u64 v = v0;
+    const u32 bi = act ? (oidx ? __ldg(oidx + i) : (u32)i) : 0xFFFFFFFFu;  // batch index
     const unsigned act_m = __ballot_sync(0xFFFFFFFFu, act);
     const unsigned same = __match_any_sync(0xFFFFFFFFu, key) & act_m;
-    const int first = __ffs(same) - 1;
-    // fold the group's values into its first lane (all lanes take part in every shuffle)
+    // the group's lowest and highest batch index, and (fold) its folded value,
+    // gathered into every member lane (all lanes take part in every shuffle)
+    u32 lo = bi, hi = act ? bi : 0u;
     for (int j = 0; j < 32; j++) {
-      const u64 vj = __shfl_sync(0xFFFFFFFFu, v, j);
-      if (act && lane == first && j != lane && ((same >> j) & 1u)) v = merge_of(merge, v, vj);
+      const u64 vj = __shfl_sync(0xFFFFFFFFu, v0, j);  // members' own values, not partial folds
+      const u32 bj = __shfl_sync(0xFFFFFFFFu, bi, j);
+      if (act && j != lane && ((same >> j) & 1u)) {
+        if (fold && j < lane) v = merge_of(merge, v, vj);
+        lo = bj < lo ? bj : lo;
+        hi = bj > hi ? bj : hi;
+      }
     }
+    // one lane per warp group talks to the table: the group's last lane,
+    // which (fold) now holds the fold of every member
+    const int last = same ? 31 - __clz(same) : -1;
     u64 h = 0;
-    if (act && lane == first) {
+    if (act && lane == last) {
       h = mix64(key ^ 0x9E3779B97F4A7C15ull) & mask;
       while (true) {
         const u64 cur = *(volatile const u64*)(tk + h);
@@ -585,29 +768,33 @@ __global__ void __launch_bounds__(256) k_agg_insert(const u64* __restrict__ keys
         }
         h = (h + 1) & mask;
       }
-      // the group's leader (the op that reports INSERTED for a new key) is its
-      // lowest batch index, as in the sequential reference order; the first
-      // lane of a warp group holds the group's lowest index
-      atomicMin(leader + h, (u32)i);
+      atomicMin(leader + h, lo);
       if (merge == M_ADD) atomicAdd((unsigned long long*)(tv + h), (unsigned long long)v);
       else if (merge == M_MAX) atomicMax((unsigned long long*)(tv + h), (unsigned long long)v);
-      else atomicMin((unsigned long long*)(tv + h), (unsigned long long)v);
+      else if (merge == M_MIN) atomicMin((unsigned long long*)(tv + h), (unsigned long long)v);
+      else if (merge == M_REPLACE) atomicMax((unsigned long long*)(tv + h), (unsigned long long)hi + 1);
     }
-    h = __shfl_sync(0xFFFFFFFFu, h, first < 0 ? 0 : first);
+    h = __shfl_sync(0xFFFFFFFFu, h, last < 0 ? 0 : last);
     if (act) grp[i] = (u32)h;
   }
 }
 
-// one group per leader op (ops, not table slots, are scanned)
-__global__ void __launch_bounds__(256) k_agg_compact(const u64* __restrict__ keys, const u32* __restrict__ grp,
-                                                     const u32* leader, const u64* tv, u64 n, u64* gkey, u64* gval,
-                                                     u32* slot2g, u64* ng) {
+// one group per leader op (ops, not table slots, are scanned).  REPLACE /
+// KEEP: the winning op's value is read back through a batch-index -> segment
+// position map (pos), the identity when the segment is in batch order.
+__global__ void __launch_bounds__(256) k_agg_compact(const u64* __restrict__ keys, const u64* __restrict__ vals,
+                                                     const u32* __restrict__ oidx, const u32* __restrict__ grp,
+                                                     const u32* leader, const u64* tv, const u32* pos, u64 n,
+                                                     const u64* dn, int merge, u64* gkey, u64* gval, u32* slot2g,
+                                                     u64* ng) {
+  n = dev_n(n, dn);
   const int lane = threadIdx.x & 31;
   for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < n;
        base += (u64)gridDim.x * blockDim.x) {
     const u64 i = base + lane;
     const u32 h = i < n ? grp[i] : 0u;
-    const bool lead = i < n && leader[h] == (u32)i;
+    const u32 bi = i < n ? (oidx ? oidx[i] : (u32)i) : 0u;
+    const bool lead = i < n && leader[h] == bi;
     const u32 m = __ballot_sync(0xFFFFFFFFu, lead);
     if (!m) continue;
     u64 at = 0;
@@ -616,24 +803,41 @@ __global__ void __launch_bounds__(256) k_agg_compact(const u64* __restrict__ key
     if (lead) {
       const u64 g = at + __popc(m & ((1u << lane) - 1));
       gkey[g] = __ldg(keys + i);
-      gval[g] = tv[h];
+      u64 v;
+      if (merge == M_KEEP) v = __ldg(vals + i);  // the leader is the first write
+      else if (merge == M_REPLACE) {
+        const u32 w = (u32)(tv[h] - 1);  // highest batch index of the group
+        v = __ldg(vals + (pos ? pos[w] : w));
+      } else v = tv[h];
+      gval[g] = v;
       slot2g[h] = (u32)g;
     }
   }
 }
 
-__global__ void k_agg_expand(const u32* grp, const u32* leader, const u32* slot2g, u64 n, const u8* gst, u8* status) {
+__global__ void k_pos_of(const u32* __restrict__ oidx, u64 n, const u64* dn, u32* pos) {
+  n = dev_n(n, dn);
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    pos[oidx[i]] = (u32)i;
+}
+
+__global__ void k_agg_expand(const u32* grp, const u32* leader, const u32* __restrict__ oidx, const u32* slot2g,
+                             u64 n, const u64* dn, const u8* gst, u8* status) {
+  n = dev_n(n, dn);
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     const u32 h = grp[i];
     const u8 gs = gst[slot2g[h]];
-    status[i] = leader[h] == (u32)i ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
+    const u32 bi = oidx ? oidx[i] : (u32)i;
+    status[i] = leader[h] == bi ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
   }
 }
 
-// one uniform upsert batch (merge = uop >> 4), combined; see above
+// one uniform upsert batch (merge = uop >> 4), combined; see above.  oidx /
+// dn / nbatch: a gathered segment (positions -> batch indices < nbatch, the
+// device-resident length dn); all null / 0 for a plain batch.
 int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status, cudaStream_t s,
-                    u32 flags, const CallCtx& cx) {
-  int rc = validate(keys, nullptr, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
+                    u32 flags, const CallCtx& cx, const u32* oidx, const u64* dn, u64 nbatch) {
+  int rc = dn ? WS_OK : validate(keys, nullptr, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
   if (rc) return rc;
   // the folded batch keeps the kernels gated on this call's validation verdict
   // (an asynchronous check is not read back here, but a batch holding a
@@ -649,64 +853,36 @@ int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n
     return p;
   };
   auto release = [&]() { for (void* p : mem) cudaFreeAsync(p, s); };
+  const u64 cap = next_pow2(n + n / 2);  // load <= 2/3; ~24 B/slot, L2-resident up to ~3M ops
   u8* gst = (u8*)alloc(n);
   u64* gkey = (u64*)alloc(8 * n);
   u64* gval = (u64*)alloc(8 * n);
   u64* ng = (u64*)alloc(8);
-  if (!gst || !gkey || !gval || !ng) { release(); return WS_ERR_ALLOC; }
+  u64* tk = (u64*)alloc(8 * cap);
+  u64* tv = (u64*)alloc(8 * cap);
+  u32* leader = (u32*)alloc(4 * cap);
+  u32* slot2g = (u32*)alloc(4 * cap);
+  u32* grp = (u32*)alloc(4 * n);
+  u32* pos = (oidx && m == M_REPLACE) ? (u32*)alloc(4 * std::max<u64>(nbatch, 1)) : nullptr;
+  if (!gst || !gkey || !gval || !ng || !tk || !tv || !leader || !slot2g || !grp || (oidx && m == M_REPLACE && !pos)) {
+    release();
+    return WS_ERR_ALLOC;
+  }
+  WS_CK(cudaMemsetAsync(tk, 0, 8 * cap, s));
+  WS_CK(cudaMemsetAsync(tv, m == M_MIN ? 0xFF : 0, 8 * cap, s));  // the merge's identity (REPLACE: no winner)
+  WS_CK(cudaMemsetAsync(leader, 0xFF, 4 * cap, s));
+  WS_CK(cudaMemsetAsync(slot2g, 0, 4 * cap, s));
+  WS_CK(cudaMemsetAsync(ng, 0, 8, s));
+  if (pos) k_pos_of<<<grid_for(n), kThreads, 0, s>>>(oidx, n, dn, pos);
+  k_agg_insert<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, n, dn, m, tk, tv, leader, cap - 1, grp);
+  k_agg_compact<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, grp, leader, tv, pos, n, dn, m, gkey, gval, slot2g,
+                                            ng);
+  rc = cuda_err(cudaGetLastError());
   CallCtx gcx = cx;
   gcx.dn = ng;  // the group count stays on the device
-  if (m == M_ADD || m == M_MAX || m == M_MIN) {
-    const u64 cap = next_pow2(n + n / 2);  // load <= 2/3; ~24 B/slot, L2-resident up to ~3M ops
-    u64* tk = (u64*)alloc(8 * cap);
-    u64* tv = (u64*)alloc(8 * cap);
-    u32* leader = (u32*)alloc(4 * cap);
-    u32* slot2g = (u32*)alloc(4 * cap);
-    u32* grp = (u32*)alloc(4 * n);
-    if (!tk || !tv || !leader || !slot2g || !grp) { release(); return WS_ERR_ALLOC; }
-    WS_CK(cudaMemsetAsync(tk, 0, 8 * cap, s));
-    WS_CK(cudaMemsetAsync(tv, m == M_MIN ? 0xFF : 0, 8 * cap, s));  // the merge's identity
-    WS_CK(cudaMemsetAsync(leader, 0xFF, 4 * cap, s));
-    WS_CK(cudaMemsetAsync(slot2g, 0, 4 * cap, s));
-    WS_CK(cudaMemsetAsync(ng, 0, 8, s));
-    k_agg_insert<<<grid_for(n), 256, 0, s>>>(keys, vals, n, m, tk, tv, leader, cap - 1, grp);
-    k_agg_compact<<<grid_for(n), 256, 0, s>>>(keys, grp, leader, tv, n, gkey, gval, slot2g, ng);
-    rc = cuda_err(cudaGetLastError());
-    if (!rc) rc = run_device_plain(t, nullptr, uop, gkey, gval, n, gst, nullptr, s, inner, false, true, false, gcx);
-    if (!rc && status) {
-      k_agg_expand<<<grid_for(n), kThreads, 0, s>>>(grp, leader, slot2g, n, gst, status);
-      rc = cuda_err(cudaGetLastError());
-    }
-    release();
-    return rc;
-  }
-  // REPLACE / KEEP: stable key sort, runs folded in index order
-  u64* sk = (u64*)alloc(8 * n);
-  u32* idx = (u32*)alloc(4 * n);
-  u32* si = (u32*)alloc(4 * n);
-  u32* head = (u32*)alloc(4 * n);
-  u32* seg = (u32*)alloc(4 * n);
-  u32* uniq = (u32*)alloc(4 * n);
-  OpVal* ov = (OpVal*)alloc(sizeof(OpVal) * n);
-  OpVal* agg = (OpVal*)alloc(sizeof(OpVal) * n);
-  if (!sk || !idx || !si || !head || !seg || !uniq || !ov || !agg) { release(); return WS_ERR_ALLOC; }
-  size_t tb = 0, tb2 = 0, tb3 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
-  cub::DeviceScan::InclusiveSum(nullptr, tb2, head, seg, (int64_t)n, s);
-  cub::DeviceReduce::ReduceByKey(nullptr, tb3, seg, uniq, ov, agg, ng, CombineOp(), (int64_t)n, s);
-  void* tmp = alloc(std::max(tb, std::max(tb2, tb3)) + 16);
-  if (!tmp) { release(); return WS_ERR_ALLOC; }
-  k_comb_iota<<<grid_for(n), kThreads, 0, s>>>(n, idx);
-  cub::DeviceRadixSort::SortPairs(tmp, tb, keys, sk, idx, si, (int64_t)n, 0, 64, s);
-  k_comb_heads<<<grid_for(n), kThreads, 0, s>>>(sk, si, uop, vals, n, head, ov);
-  cub::DeviceScan::InclusiveSum(tmp, tb2, head, seg, (int64_t)n, s);
-  cub::DeviceReduce::ReduceByKey(tmp, tb3, seg, uniq, ov, agg, ng, CombineOp(), (int64_t)n, s);
-  k_comb_groups<<<grid_for(n), kThreads, 0, s>>>(sk, head, seg, n, gkey);
-  k_comb_vals<<<grid_for(n), kThreads, 0, s>>>(agg, ng, n, gval);
-  rc = cuda_err(cudaGetLastError());
   if (!rc) rc = run_device_plain(t, nullptr, uop, gkey, gval, n, gst, nullptr, s, inner, false, true, false, gcx);
   if (!rc && status) {
-    k_comb_expand<<<grid_for(n), kThreads, 0, s>>>(si, head, seg, n, gst, status);
+    k_agg_expand<<<grid_for(n), kThreads, 0, s>>>(grp, leader, oidx, slot2g, n, dn, gst, status);
     rc = cuda_err(cudaGetLastError());
   }
   release();
@@ -724,7 +900,7 @@ int run_device(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* v
   if (ops)  // split by op byte; each upsert segment is combined (run_device_by_kind)
     return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, cx);
   if (vout) WS_CK(cudaMemsetAsync(vout, 0, 8 * n, s));
-  return combine_uniform(t, uop, keys, vals, n, status, s, flags, cx);
+  return combine_uniform(t, uop, keys, vals, n, status, s, flags, cx, nullptr, nullptr, 0);
 }
 
 // Host-buffer batches: staged through device memory in 4M-op chunks on three

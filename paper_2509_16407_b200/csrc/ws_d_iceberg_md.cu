@@ -152,7 +152,147 @@ __global__ void __launch_bounds__(256) k_upsert_icemd_rounds(Dev d, const u64* _
   }
 }
 
+// Iceberg-MD query (reference openaddr.py:593-610, Ctx::ice_find with the
+// early exit), one thread per op with the pair-cooperative 64-byte tag
+// fetches of k_query_p2md_coop: front bucket tags -> confirm; a front with a
+// zero tag while the table never tombstoned proves the key never reached the
+// backyard (early exit); else both backyard buckets, b2 only when b2 != b1.
+template <bool RO, bool F64>
+__global__ void __launch_bounds__(256) k_query_icemd_coop(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
+                                                          u8* found, int conc_erase, int gated) {
+  WS_PROLOGUE(d, gated, n);
+  const u32 te0 = ld_u32_relaxed(d.state);
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 first = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull;  // warp-uniform loop bound
+  for (u64 base = first; base < n; base += stride) {
+    const u64 i = base + (threadIdx.x & 31);
+    const bool act = i < n;
+    const u64 key = act ? __ldg(keys + i) : 0;
+    const u64 h0 = mix64(key ^ d.seeds[0]);
+    const u64 b0 = d.frontm(h0 >> 16);
+    const u16 t = (u16)(h0 & 0xFFFF);
+    const u16 tag = t ? t : (u16)1;
+    u32 M, Z;
+    coop_masks<RO, F64>(d, act, b0, tag, M, Z);
+    u64 val = 0;
+    bool hit = act && M && pair_confirm<RO, F64>(d, b0, M, key, val) >= 0;
+    bool te = te0 != 0;
+    if (conc_erase) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
+    const u64 b1 = d.front + d.backm(mix64(key ^ d.seeds[1]) >> 16);
+    const u64 b2 = d.front + d.backm(mix64(key ^ d.seeds[2]) >> 16);
+    const bool need1 = act && !hit && !(Z && !te);
+    if (__any_sync(0xFFFFFFFFu, need1)) {
+      coop_masks<RO, F64>(d, need1, b1, tag, M, Z);
+      if (need1 && M) hit = pair_confirm<RO, F64>(d, b1, M, key, val) >= 0;
+      const bool need2 = need1 && !hit && b2 != b1;
+      if (__any_sync(0xFFFFFFFFu, need2)) {
+        coop_masks<RO, F64>(d, need2, b2, tag, M, Z);
+        if (need2 && M) hit = pair_confirm<RO, F64>(d, b2, M, key, val) >= 0;
+      }
+    }
+    if (act) {
+      if (found) found[i] = hit;
+      if (vout) vout[i] = hit ? val : 0;
+    }
+  }
+}
+
+// Iceberg-MD erase (reference openaddr.py:612-631, Ctx::ice_erase): the
+// front lock only, as the reference; warp-synchronous lock rounds with
+// non-blocking try-locks, the ice_find search above with coherent loads, and
+// the tombstone protocol of Ctx::tombstone (tombstones_ever set, fence, cell
+// := TOMB, fence, tag := 0) with one fence per step for the whole warp.
+template <bool F64>
+__global__ void __launch_bounds__(256) k_erase_icemd_rounds(Dev d, const u64* __restrict__ keys, u64 n,
+                                                            u8* found, int conc_erase, int gated) {
+  WS_PROLOGUE(d, gated, n);
+  const int lane = threadIdx.x & 31;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 c = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; c * 32 < n; c += nwarps) {
+    const u64 i = c * 32 + lane;
+    bool pending = i < n;
+    const u64 key = pending ? __ldg(keys + i) : 0;
+    const u64 h0 = mix64(key ^ d.seeds[0]);
+    const u64 b0 = d.frontm(h0 >> 16);
+    const u16 t = (u16)(h0 & 0xFFFF);
+    const u16 tag = t ? t : (u16)1;
+    const u64 b1 = d.front + d.backm(mix64(key ^ d.seeds[1]) >> 16);
+    const u64 b2 = d.front + d.backm(mix64(key ^ d.seeds[2]) >> 16);
+    bool gone = false, held = false;
+    unsigned backoff = 64;
+    while (__any_sync(0xFFFFFFFFu, pending)) {
+      if (pending && !held) held = try_lock_bucket(d.locks, b0);
+      const bool hold = pending && held;
+      u32 M, Z;
+      coop_masks<false, F64>(d, hold, b0, tag, M, Z);
+      i64 slot = -1;
+      u64 v;
+      if (hold && M) {
+        const int j = pair_confirm<false, F64>(d, b0, M, key, v);
+        if (j >= 0) slot = (i64)(b0 * 32 + j);
+      }
+      bool te = true;
+      if (__any_sync(0xFFFFFFFFu, hold && slot < 0)) {
+        fence_acq_rel();  // as Ctx::tomb_ever under concurrent erases
+        te = ld_u32_relaxed(d.state) != 0;
+      }
+      const bool need1 = hold && slot < 0 && !(Z && !te);
+      if (__any_sync(0xFFFFFFFFu, need1)) {
+        coop_masks<false, F64>(d, need1, b1, tag, M, Z);
+        if (need1 && M) {
+          const int j = pair_confirm<false, F64>(d, b1, M, key, v);
+          if (j >= 0) slot = (i64)(b1 * 32 + j);
+        }
+        const bool need2 = need1 && slot < 0 && b2 != b1;
+        if (__any_sync(0xFFFFFFFFu, need2)) {
+          coop_masks<false, F64>(d, need2, b2, tag, M, Z);
+          if (need2 && M) {
+            const int j = pair_confirm<false, F64>(d, b2, M, key, v);
+            if (j >= 0) slot = (i64)(b2 * 32 + j);
+          }
+        }
+      }
+      // tombstone protocol, one fence per step for the warp
+      const bool del = slot >= 0;
+      if (__any_sync(0xFFFFFFFFu, del)) {
+        if (del && ld_u32_relaxed(d.state) == 0) st_u32_relaxed(d.state, 1u);
+        fence_acq_rel();
+        if (del) st_cell(d.cells + 2 * (u64)slot, TOMB, 0);
+        fence_acq_rel();  // the tombstone is visible before the zero tag that advertises it
+        if (del) st_tag(d.tags + (u64)slot, 0);
+      }
+      if (hold) {
+        gone = del;
+        pending = false;
+      }
+      __syncwarp();
+      fence_acq_rel();
+      if (held && !pending) {
+        red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+        held = false;
+      }
+      if (pending) {
+        __nanosleep(backoff + 8 * lane);
+        if (backoff < 4096) backoff <<= 1;
+      }
+    }
+    if (i < n && found) found[i] = gone;
+  }
+}
+
 static void iceberg_md_ops(const OpsArgs& a, bool def) {
+  const bool erase_only = !a.ops && (a.uop & 15) == OP_ERASE;
+  if (def && erase_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && !a.d.phased &&
+      a.d.tune_upsert == 4) {
+    u64 g = (a.n + 255) / 256;
+    const u64 lim = std::max<u64>((a.d.front + 255) / 256, 4);  // <= ~1 op in flight per front bucket
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
+    if (a.d.tune_l2pol == 2)
+      k_erase_icemd_rounds<true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.status, a.conc_erase, a.gated);
+    else
+      k_erase_icemd_rounds<false><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.status, a.conc_erase, a.gated);
+    return;
+  }
   const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
   if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && !a.d.phased && !a.d.lock_elided &&
       a.d.tune_upsert == 4) {
@@ -166,6 +306,17 @@ static void iceberg_md_ops(const OpsArgs& a, bool def) {
   if (def) launch_ops_t<D_ICEBERG_MD, 32>(a); else launch_ops_t<D_ICEBERG_MD, 0>(a);
 }
 static void iceberg_md_query(const QueryArgs& a, bool def) {
+  if (def && a.d.tune_qilp > 0) {
+    u64 g = (a.n + 255) / 256;
+    g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * 8);
+#define WS_QI(RO, F) k_query_icemd_coop<RO, F><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, \
+                                                                            a.conc_erase, a.gated)
+    const bool f64 = a.d.tune_l2pol == 2;
+    if (a.ro) { if (f64) WS_QI(true, true); else WS_QI(true, false); }
+    else { if (f64) WS_QI(false, true); else WS_QI(false, false); }
+#undef WS_QI
+    return;
+  }
   if (def) launch_query_t<D_ICEBERG_MD, 32>(a); else launch_query_t<D_ICEBERG_MD, 0>(a);
 }
 static void iceberg_md_locate(const LocateArgs& a, bool def) {
@@ -175,6 +326,9 @@ static void iceberg_md_preload(bool def) {
   if (!def) { preload_t<D_ICEBERG_MD, 0>(); return; }
   preload_t<D_ICEBERG_MD, 32>();
   preload_fn(k_upsert_icemd_rounds<true>);
+  preload_fn(k_query_icemd_coop<false, true>);
+  preload_fn(k_query_icemd_coop<true, true>);
+  preload_fn(k_erase_icemd_rounds<true>);
 }
 Launchers launchers_iceberg_md() {
   return Launchers{iceberg_md_ops, iceberg_md_query, iceberg_md_locate, iceberg_md_preload};

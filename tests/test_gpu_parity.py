@@ -445,11 +445,14 @@ def test_combined_hot_key_batch_matches_oracle(design, merge):
         o = _oracle(cfg)
         o.upsert_batch(keys, vals, merge)
         assert got == o.as_dict()
-    else:  # keep / replace: each key holds one of its batch values
-        per = {}
+    else:  # keep / replace: the first / last write of batch-index order wins
+        want = {}
         for k, v in zip(keys.tolist(), vals.tolist()):
-            per.setdefault(k, set()).add(v)
-        assert set(got) == set(per) and all(got[k] in per[k] for k in got)
+            if merge is None or k not in want:
+                want[k] = v
+        assert got == want
+        # and the INSERTED status goes to each key's first op
+        assert (st[first] == 0).all()
     assert t.duplicate_scan() == {}
 
 
