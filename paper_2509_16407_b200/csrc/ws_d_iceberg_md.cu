@@ -306,7 +306,9 @@ static void iceberg_md_ops(const OpsArgs& a, bool def) {
   if (def) launch_ops_t<D_ICEBERG_MD, 32>(a); else launch_ops_t<D_ICEBERG_MD, 0>(a);
 }
 static void iceberg_md_query(const QueryArgs& a, bool def) {
-  if (def && a.d.tune_qilp > 0) {
+  // opt-in (query_ilp = 6): the pair-cooperative query measured slower than
+  // the generic one at 2^26, where the tag array is largely L2-resident
+  if (def && a.d.tune_qilp == 6) {
     u64 g = (a.n + 255) / 256;
     g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * 8);
 #define WS_QI(RO, F) k_query_icemd_coop<RO, F><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, \
