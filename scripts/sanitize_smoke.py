@@ -69,6 +69,28 @@ def main():
     t.mixed_batch(cu(ops), cu(k), cu(np.ones(70_000, U64)))
     o.mixed_batch(ops, k, np.ones(70_000, U64))
     assert dict(t.items()) == o.as_dict()
+    # the sort-free split (erase / query / rest regions) with combining of
+    # duplicate ADD and REPLACE upserts, and the tuned iceberg_md erase
+    for d in ("iceberg_md", "p2_md"):
+        cfg = cfg_for(d, 1 << 18, seed=7)
+        t, o = make_table(cfg), OracleTable(cfg)
+        base = gen_uniform_keys(23, 150_000)
+        t.upsert_batch(cu(base), cu(base))
+        o.upsert_batch(base, base)
+        rng = np.random.default_rng(1)
+        hot = gen_uniform_keys(24, 2000)
+        ops = np.concatenate([np.full(20_000, 1), np.full(20_000, 2), np.full(20_000, 2 << 4),
+                              np.full(20_000, 0)]).astype(np.uint8)
+        keys = np.concatenate([base[:20_000], base[20_000:40_000], hot[rng.integers(0, 1000, 20_000)],
+                               hot[1000 + rng.integers(0, 1000, 20_000)]])
+        vals = rng.integers(1, 1 << 40, len(keys)).astype(U64)
+        perm = rng.permutation(len(keys))
+        ops, keys, vals = ops[perm], keys[perm], vals[perm]
+        st, vo = t.mixed_batch(cu(ops), cu(keys), cu(vals), combine=True)
+        ost, ovo = o.mixed_batch(ops, keys, vals)
+        assert (st.cpu().numpy() == ost).all() and (vo.cpu().view(torch.int64).numpy().view(U64) == ovo).all(), d
+        assert dict(t.items()) == o.as_dict(), d
+        print("ok split+combine", d, flush=True)
     torch.cuda.synchronize()
     print("sanitize smoke ok", flush=True)
 
