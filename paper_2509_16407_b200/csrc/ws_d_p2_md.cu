@@ -95,7 +95,7 @@ static void p2_md_query(const QueryArgs& a, bool def) {
   if (a.ro) { if (f64) WS_QC(true, true, MB); else WS_QC(true, false, MB); } \
   else { if (f64) WS_QC(false, true, MB); else WS_QC(false, false, MB); }
       const bool f64 = a.d.tune_l2pol == 2;
-      if (a.d.tune_occ == 8) { WS_QC2(8) } else if (a.d.tune_occ == 6) { WS_QC2(6) } else { WS_QC2(1) }
+      if (a.d.tune_occ == 8) { WS_QC2(8) } else { WS_QC2(1) }
 #undef WS_QC2
 #undef WS_QC
       break;
