@@ -165,7 +165,9 @@ WS_API int ws_info(ws_table *t, ws_info_t *info);
 #define WS_TUNE_L2_POLICY 2 /* 1: tag loads L2 evict_last, cell loads evict_first; 2: 64-byte L2 fills */
 #define WS_TUNE_UPSERT 3    /* P2-MD upsert: 0 one thread per op, 1 lane-pair tiles,
                                2 warp-synchronous lock rounds, 3 rounds + 64-byte L2 fills,
-                               4 = 3 + full-sector cell writes when the partner cell is EMPTY (default) */
+                               4 = 3 + full-sector cell writes when the partner cell is EMPTY (default);
+                               cuckoo: 4 = lock rounds + cooperative 8-lane eviction launch (default),
+                               6 = lock rounds + one-thread-per-op eviction launch */
 #define WS_TUNE_OCCUPANCY 4 /* tuned kernels: request >= value CTAs/SM from ptxas (0 = compiler choice) */
 /* race-window widening for the adversarial duplicate-key test (reference
  * bench/adversarial.py:40-93 DelayProfile): at the hook stages pre_reserve,

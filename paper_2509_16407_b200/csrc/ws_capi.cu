@@ -1564,7 +1564,7 @@ int ws_tune(ws_table* t, int knob, int value) {
       t->d.tune_pf = value;
       return WS_OK;
     case WS_TUNE_UPSERT:
-      if (value < 0 || value > 5) return WS_ERR_ARG;
+      if (value < 0 || value > 6) return WS_ERR_ARG;
       t->d.tune_upsert = value;
       return WS_OK;
     default: return WS_ERR_ARG;

@@ -257,9 +257,144 @@ __global__ void __launch_bounds__(256) k_compact_retry(const u8* __restrict__ st
   }
 }
 
+// Eviction launch (the S_RETRY ops of k_upsert_cuckoo_rounds, compacted),
+// one op per 8-lane group, 4 ops per warp.  Exactly Ctx::ck_upsert with
+// ck_resume (reference cuckoo.py:58-105) except that its depth-1 path search
+// (Ctx::ck_find_path1: start buckets in order, their resident slots in order,
+// seeds in order, the first alternate with a free cell wins) runs across the
+// group: lane j loads slot j of every start bucket, then the candidates
+// (bucket, slot, seed) are checked in the serial order in waves of 8, one
+// alternate per lane (whole-line key loads), and the first wave holding a
+// free alternate yields its lowest-order one -- the path the serial search
+// returns: duplicates of an earlier alternate are free exactly when it is, so
+// skipping them (the serial seen-set) cannot change the first free one.  Locked scans, moves and the full BFS fallback
+// run on the group's leader lane with the generic code.
+__device__ __forceinline__ bool line8_has_free(const u64* line) {
+  bool f = false;
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    u64 a, b, c, e;
+    asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(e) : "l"(line + 4 * q) : "memory");
+    f |= free_key(a) | free_key(c);
+  }
+  return f;
+}
+
+__global__ void __launch_bounds__(256) k_ck_evict_coop(Dev d, const u64* __restrict__ keys,
+                                                       const u64* __restrict__ vals, int merge, u8* status,
+                                                       const u32* __restrict__ rlist, const u32* rcount,
+                                                       int conc_erase) {
+  Ctx<D_CUCKOO, 8, false, false> c{d, nullptr, conc_erase != 0, ld_u32_relaxed(d.state)};
+  const int lane = threadIdx.x & 31, lj = lane & 7, lead = lane & ~7;
+  const unsigned gm = 0xFFu << lead;
+  const bool leader = lj == 0;
+  const u64 ngroups = ((u64)gridDim.x * blockDim.x) >> 3;
+  const u32 cnt = *rcount;
+  for (u64 t = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 3; t < cnt; t += ngroups) {
+    const u32 i = rlist[t];
+    const u64 key = keys[i], val = vals[i];
+    u64 uq[8];
+    const int nu = c.ck_buckets(key, uq);
+    u8 st = 0xFF;
+    bool final_scan = false;
+    for (int attempt = 0; attempt < CUCKOO_RETRIES; attempt++) {
+      if (attempt > 0 || !d.ck_resume) {  // locked scan of the op's own buckets (leader)
+        int code = 0;                     // 1: decided (st), 2: lost a race for a free cell
+        if (leader) {
+          c.ck_lock_all(uq, nu);
+          i64 free_at = -1;
+          for (int b = 0; b < nu && st == 0xFF; b++) {
+            Find r = c.scan_cells(uq[b] * 8, 8, key);
+            if (r.idx >= 0) st = c.update(r.idx, key, r.val, val, merge);
+            else if (free_at < 0 && r.hint >= 0) free_at = r.hint;
+          }
+          if (st == 0xFF && free_at >= 0 && publish_cell(c.cell((u64)free_at), key, val)) st = S_INSERTED;
+          c.ck_unlock_all(uq, nu);
+          code = st != 0xFF ? 1 : free_at >= 0 ? 2 : 0;
+        }
+        code = __shfl_sync(gm, code, lead);
+        if (code == 1) break;
+        if (code == 2) continue;
+        if (final_scan) { st = S_FULL; break; }
+      }
+      if (d.depth >= 1 && nu <= 3 && d.ways == 3) {
+        // resident keys: lane j holds slot j of every start bucket
+        u64 k[3];
+#pragma unroll
+        for (int b = 0; b < 3; b++) {
+          k[b] = 0;
+          if (b < nu) { u64 v; c.ldc(uq[b] * 8 + lj, k[b], v); }
+        }
+        // candidates in the serial search's order c = (bucket * 8 + slot) * 3 + seed,
+        // checked in waves of 8 (one per lane) until a wave holds a free alternate
+        int found = -1;
+        u64 falt = 0, fkey = 0;
+        for (int w = 0; w < nu * 3 && found < 0; w++) {
+          const int cidx = 8 * w + lj, b = cidx / 24, slot = (cidx % 24) / 3, sd = cidx % 3;
+          const u64 k0 = __shfl_sync(gm, k[0], lead + slot), k1 = __shfl_sync(gm, k[1], lead + slot),
+                    k2 = __shfl_sync(gm, k[2], lead + slot);
+          const u64 kk = b == 0 ? k0 : b == 1 ? k1 : k2;
+          bool fr = false;
+          u64 alt = 0;
+          if (b < nu && !free_key(kk) && kk < RESV) {
+            alt = c.hb(sd, kk, d.nbm);
+            bool dup = false;
+            for (int q = 0; q < nu; q++) dup |= alt == uq[q];
+            fr = !dup && line8_has_free(d.cells + 16 * alt);
+          }
+          const unsigned m = __ballot_sync(gm, fr) & gm;
+          if (m) {
+            const int src = __ffs(m) - 1;
+            found = __shfl_sync(gm, b * 8 + slot, src);
+            falt = __shfl_sync(gm, alt, src);
+            fkey = __shfl_sync(gm, kk, src);
+          }
+        }
+        if (found >= 0) {
+          if (leader) {
+            const int b = found / 8, slot = found % 8;
+            const u64 mv[4] = {uq[b], uq[b] * 8 + (u64)slot, fkey, falt};
+            c.ck_execute(mv, 1);  // a failed move means the world changed: retry
+          }
+          __syncwarp(gm);
+          continue;
+        }
+      } else if (d.depth >= 1) {  // more than three distinct buckets: the serial depth-1 search
+        int r1 = 0;
+        if (leader) {
+          u64 mv1[4];
+          r1 = c.ck_find_path1(uq, nu, mv1);
+          if (r1 == 1) c.ck_execute(mv1, 1);
+        }
+        r1 = __shfl_sync(gm, r1, lead);
+        if (r1 == 1) continue;
+      }
+      int len = 0;
+      if (leader) {
+        u32 wid;
+        u64* ws = c.ws_acquire(wid);
+        len = c.ck_find_path(ws, uq, nu);
+        if (len > 0) c.ck_execute(ws + 4 * (d.bfs_entries - (u64)len), len);
+        c.ws_release(wid);
+      }
+      len = __shfl_sync(gm, len, lead);
+      if (len < 0) {
+        if (attempt == 0 && d.ck_resume) { final_scan = true; continue; }
+        st = S_FULL;
+        break;
+      }
+    }
+    if (st == 0xFF) st = S_FULL;
+    if (leader && status) status[i] = st;
+  }
+}
+
 static void cuckoo_ops(const OpsArgs& a, bool def) {
   const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
-  if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && a.d.ways <= 8 && a.d.tune_upsert == 4) {
+  // tune_upsert 6: the same fast path with the round-1 one-thread-per-op eviction launch (A/B)
+  if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && a.d.ways <= 8 &&
+      (a.d.tune_upsert == 4 || a.d.tune_upsert == 6)) {
     u8* st = a.status;
     if (!st && cudaMallocAsync((void**)&st, a.n, a.s) != cudaSuccess) st = nullptr;
     if (st) {
@@ -281,7 +416,14 @@ static void cuckoo_ops(const OpsArgs& a, bool def) {
         lo.rlist = rl;
         lo.rcount = rl + a.n;
       }
-      launch_ops_t<D_CUCKOO, 8>(lo);
+      if (rl && a.vals && a.d.tune_upsert == 4) {
+        // 8 lanes per op; the grid covers the worst case (every op retries)
+        const u64 g = std::max<u64>(std::min<u64>((8 * a.n + 255) / 256, (u64)kSMs * 8), 1);
+        k_ck_evict_coop<<<(unsigned)g, 256, 0, a.s>>>(lo.d, a.keys, a.vals, a.uop >> 4, st, rl, rl + a.n,
+                                                      a.conc_erase);
+      } else {
+        launch_ops_t<D_CUCKOO, 8>(lo);
+      }
       if (rl) cudaFreeAsync(rl, a.s);
       if (st != a.status) cudaFreeAsync(st, a.s);
       return;
@@ -311,6 +453,7 @@ static void cuckoo_preload(bool def) {
   preload_fn(k_query_cuckoo_rounds<8>);
   preload_fn(k_upsert_cuckoo_rounds);
   preload_fn(k_compact_retry);
+  preload_fn(k_ck_evict_coop);
 }
 Launchers launchers_cuckoo() { return Launchers{cuckoo_ops, cuckoo_query, cuckoo_locate, cuckoo_preload}; }
 
