@@ -87,6 +87,10 @@ enum { WS_OP_UPSERT = 0, WS_OP_ERASE = 1, WS_OP_QUERY = 2 };
                                (hot-key / Zipf batches); statuses as if applied in some order */
 #define WS_F_INTERLEAVED 16u /* mixed batch: keep every op kind in ONE interleaved launch (race tests);
                                default: large mixed batches run as per-kind segments */
+#define WS_F_CONCURRENT_KINDS 32u /* mixed batch: run the per-kind segments CONCURRENTLY (erases,
+                               queries and upserts on three streams forked from the caller's,
+                               joined before return) with the tuned kernels, so erases race
+                               inserts and queries as in the reference's threaded aging */
 
 /* All derived integers are computed by the host layer exactly as the
  * reference computes them (core.py:209-211, openaddr.py:45-47,351-352,505-507). */

@@ -27,6 +27,7 @@ WS_F_NO_CHECK = 2
 WS_F_SERIAL = 4
 WS_F_COMBINE = 8
 WS_F_INTERLEAVED = 16
+WS_F_CONCURRENT_KINDS = 32
 
 EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_erase", "ws_mixed",
            "ws_locate", "ws_probe_counts", "ws_occupied", "ws_export_items",

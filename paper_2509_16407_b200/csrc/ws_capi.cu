@@ -334,6 +334,7 @@ __global__ void k_comb_iota(u64 n, u32* idx);
 // internal flags of run_device_plain
 constexpr u32 kF_VALIDATED = 1u << 30;  // the caller validated the batch; keep the kernels gated
 constexpr u32 kF_NO_KIND_SORT = 1u << 29;
+constexpr u32 kF_CONC_ERASE = 1u << 28;  // other launches of this call may erase concurrently
 
 __global__ void k_kind_gather(const u32* __restrict__ perm, const u64* __restrict__ keys,
                               const u64* __restrict__ vals, u64 n, u64* kp, u64* vp) {
@@ -508,9 +509,17 @@ int run_device_split(ws_table* t, const u8* ops, const u64* keys, const u64* val
   u32* H = (u32*)carve(4 * nh); u32* S = (u32*)carve(4 * nh);
   u64* starts = (u64*)carve(257 * 8); u64* cnt = (u64*)carve(3 * 8);
   void* tmp = carve(tb + 16);
-  const u32 inner = (flags & ~(WS_F_SYNC_CHECK | WS_F_COMBINE)) | kF_NO_KIND_SORT |
-                    ((flags & WS_F_NO_CHECK) ? 0u : (kF_VALIDATED | WS_F_NO_CHECK));
+  // WS_F_CONCURRENT_KINDS: erases on se, queries on sq, upserts on s, all
+  // concurrent; every segment launch then assumes concurrent erases (the
+  // tombstone flag re-read behind a fence, as for multi_stream tables)
+  const bool par = (flags & WS_F_CONCURRENT_KINDS) != 0;
+  const u32 inner = (flags & ~(WS_F_SYNC_CHECK | WS_F_COMBINE | WS_F_CONCURRENT_KINDS)) | kF_NO_KIND_SORT |
+                    ((flags & WS_F_NO_CHECK) ? 0u : (kF_VALIDATED | WS_F_NO_CHECK)) | (par ? kF_CONC_ERASE : 0u);
   const bool comb = (flags & WS_F_COMBINE) != 0;
+  Staging* sg = par ? staging(t->device) : nullptr;
+  if (par && !sg) { cudaFreeAsync(buf, s); return WS_ERR_ALLOC; }
+  cudaStream_t se = par ? sg->s_in : s, sq = par ? sg->s_aux : s;
+  cudaEvent_t ev_fork = nullptr, ev_e = nullptr, ev_q = nullptr;
   k_kind_hist<<<nblk, kKindTile, 0, s>>>(ops, n, H);
   cub::DeviceScan::ExclusiveSum(tmp, tb, H, S, (int64_t)nh, s);
   k_kind_split<<<nblk, kKindTile, 0, s>>>(ops, keys, vals, n, S, o);
@@ -522,17 +531,26 @@ int run_device_split(ws_table* t, const u8* ops, const u64* keys, const u64* val
   if (!rc) rc = cuda_err(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   if (!rc) rc = cuda_err(cudaMemcpyAsync(hst, starts, 257 * 8, cudaMemcpyDeviceToHost, s));
   if (!rc) rc = cuda_err(cudaEventRecord(ev, s));
+  if (par && !rc) {
+    for (cudaEvent_t* e : {&ev_fork, &ev_e, &ev_q})
+      if (!rc) rc = cuda_err(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    if (!rc) rc = cuda_err(cudaEventRecord(ev_fork, s));
+    if (!rc) rc = cuda_err(cudaStreamWaitEvent(se, ev_fork, 0));
+    if (!rc) rc = cuda_err(cudaStreamWaitEvent(sq, ev_fork, 0));
+  }
   // erases and queries at once, their counts read on the device
   if (!rc) {
     CallCtx ce = cx;
     ce.dn = cnt;
-    rc = run_device_plain(t, nullptr, OP_ERASE, o.ke, nullptr, n, ste, nullptr, s, inner, true, false, false, ce);
+    rc = run_device_plain(t, nullptr, OP_ERASE, o.ke, nullptr, n, ste, nullptr, se, inner, true, false, false, ce);
   }
   if (!rc) {
     CallCtx cq = cx;
     cq.dn = cnt + 1;
-    rc = run_device_plain(t, nullptr, OP_QUERY, o.kq, nullptr, n, stq, voq, s, inner, false, false, true, cq);
+    rc = run_device_plain(t, nullptr, OP_QUERY, o.kq, nullptr, n, stq, voq, sq, inner, par, false, true, cq);
   }
+  if (par && !rc) rc = cuda_err(cudaEventRecord(ev_e, se));
+  if (par && !rc) rc = cuda_err(cudaEventRecord(ev_q, sq));
   if (!rc) rc = cuda_err(cudaEventSynchronize(ev));
   std::vector<u64> st_h(257, 0);
   if (!rc) std::copy(hst, hst + 257, st_h.begin());
@@ -548,18 +566,23 @@ int run_device_split(ws_table* t, const u8* ops, const u64* keys, const u64* val
       rc = comb && m >= 2 ? combine_uniform(t, (u8)v, o.kr + lo, o.vr + lo, m, str + lo, s, inner, cx, o.ir + lo,
                                             nullptr, n)
                           : run_device_plain(t, nullptr, (u8)v, o.kr + lo, o.vr + lo, m, str + lo, nullptr, s, inner,
-                                             false, true, false, cx);
+                                             par, true, false, cx);
     } else {  // erase / query bytes with stray merge bits, invalid bytes (gated): the generic kernel
-      rc = run_device_plain(t, o.opr + lo, 0, o.kr + lo, o.vr + lo, m, str + lo, vor + lo, s, inner, has_erase,
-                            has_upsert, false, cx);
+      rc = run_device_plain(t, o.opr + lo, 0, o.kr + lo, o.vr + lo, m, str + lo, vor + lo, s, inner,
+                            has_erase || par, has_upsert, false, cx);
     }
+  }
+  if (par) {  // join the side streams before the results are gathered (and before any error return)
+    if (ev_e) cudaStreamWaitEvent(s, ev_e, 0);
+    if (ev_q) cudaStreamWaitEvent(s, ev_q, 0);
   }
   if (!rc) {
     dim3 g(grid_for(n), 3);
     k_kind_unsplit<<<g, kThreads, 0, s>>>(cnt, o.ie, ste, o.iq, stq, voq, o.ir, str, vor, o.opr, status, vout);
     rc = cuda_err(cudaGetLastError());
   }
-  if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t e : {ev, ev_fork, ev_e, ev_q})
+    if (e) cudaEventDestroy(e);
   cudaFreeAsync(buf, s);
   return rc;
 }
@@ -645,8 +668,8 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
   if (rc) return rc;
   if (!n) return WS_OK;
   const int gated = (flags & kF_VALIDATED) ? 1 : (flags & WS_F_NO_CHECK) ? 0 : 1;
-  int conc = (has_erase || t->cfg.multi_stream) ? 1 : 0;
-  if (ops && !t->cfg.multi_stream && !(flags & WS_F_SERIAL)) {
+  int conc = (has_erase || t->cfg.multi_stream || (flags & kF_CONC_ERASE)) ? 1 : 0;
+  if (ops && !t->cfg.multi_stream && !(flags & (WS_F_SERIAL | kF_CONC_ERASE))) {
     // let the device decide: conc_erase = 2 reads the erase count at launch
     WS_CK(cudaMemsetAsync(cx.cs + 3, 0, sizeof(u32), s));
     k_count_erases<<<grid_for(n, kThreads, 4), kThreads, 0, s>>>(ops, n, cx.cs);

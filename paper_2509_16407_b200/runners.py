@@ -362,7 +362,7 @@ def _probe_means(t, ops, keys, vals, kinds, serial=False):
 
 def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_fraction: float = 0.01,
                       seed: int = 42, probe_sample: int = 200, line_bytes: int = 128,
-                      out_dir: str | None = None, interleaved: bool = False) -> dict:
+                      out_dir: str | None = None, interleaved: bool = False, concurrent: bool = False) -> dict:
     """The reference's aging workload restated (bench/runners.py:259-353):
     fill to 85%, then per iteration one concurrent mixed launch that inserts
     a 1% slice of new keys (value k & 0xFFFF), erases the oldest 1%, queries
@@ -373,8 +373,9 @@ def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_f
     reference's single-threaded recorder).  Every result is checked.
     interleaved=True runs each mixed batch as ONE launch with the kinds
     interleaved (WS_F_INTERLEAVED), so erases race inserts and queries inside
-    the kernel as the reference's threads do; the default runs the per-kind
-    segments (one serial order of the batch)."""
+    the kernel as the reference's threads do; concurrent=True runs the
+    per-kind segments concurrently on three streams with the tuned kernels;
+    the default runs them one after another (one serial order of the batch)."""
     from .tables import OP_ERASE, OP_QUERY, OP_UPSERT, make_table
     t = make_table(TableConfig(design=design, capacity_slots=capacity, seed=seed, line_bytes=line_bytes))
     dev = t.device
@@ -403,7 +404,8 @@ def run_aging_uniform(design: str, capacity: int, iterations: int = 200, slice_f
         d_ops, d_keys, d_vals = _dev(ops, dev), _dev(keys, dev), _dev(vals, dev)
         with _ncu_range({"design": design, "op": "mixed", "load": round(fill_n / cap, 4), "iteration": it},
                         len(ops)), _Timer() as tm:
-            s, _v = t.mixed_batch(d_ops, d_keys, d_vals, check=False, interleaved=interleaved)
+            s, _v = t.mixed_batch(d_ops, d_keys, d_vals, check=False, interleaved=interleaved,
+                                  concurrent=concurrent)
         s = _np(s)
         ok = bool((s[kinds == 0] == 0).all() and (s[kinds == 1] == 1).all() and
                   (s[kinds == 2] == 1).all() and not s[kinds == 3].any())

@@ -468,12 +468,15 @@ class HashTable:
         self._check(self._lib.ws_erase(self._h, kp, len(k), found.data_ptr(), self._stream(), fl))
         return as_bool(found)
 
-    def mixed_batch(self, ops, keys, values=None, check=True, serial=False, combine=False, interleaved=False):
+    def mixed_batch(self, ops, keys, values=None, check=True, serial=False, combine=False, interleaved=False,
+                    concurrent=False):
         """A concurrent batch of mixed ops (byte = kind | merge << 4, kind 0
         upsert / 1 erase / 2 query).  Returns (status uint8, values uint64):
         upsert status, erase/query found flag, query value.  Large batches run
-        as per-kind segment launches; interleaved=True keeps all kinds in one
-        launch (race tests that need erases concurrent with inserts)."""
+        as per-kind segment launches, one after another; concurrent=True runs
+        those segments concurrently on three streams (erases racing inserts
+        and queries, tuned kernels); interleaved=True keeps all kinds in one
+        generic launch (race tests that need kinds mixed inside a warp)."""
         torch = _torch()
         o, op, _oc = _as_u8(ops, torch)
         k, kp, kc = _as_u64(keys, torch)
@@ -490,6 +493,8 @@ class HashTable:
             fl |= _native.WS_F_COMBINE
         if interleaved:
             fl |= _native.WS_F_INTERLEAVED
+        if concurrent:
+            fl |= _native.WS_F_CONCURRENT_KINDS
         self._check(self._lib.ws_mixed(self._h, op, kp, vp, len(k), st.data_ptr(), vo.data_ptr(),
                                        self._stream(), fl))
         return st, vo

@@ -649,3 +649,72 @@ def test_combined_mixed_batch_matches_sequential_oracle(design, with_replace):
     assert bad.size == 0, [(int(ops[i]), int(_np(st)[i]), int(ost[i])) for i in bad[:10]]
     assert dict(t.items()) == o.as_dict()
     assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "double", "cuckoo", "chaining"])
+@pytest.mark.parametrize("combine", [False, True])
+def test_concurrent_kinds_matches_oracle(design, combine):
+    """WS_F_CONCURRENT_KINDS (mixed_batch(concurrent=True)): the erase, query
+    and upsert segments of a >= 2^16-op batch run concurrently on three
+    streams with the tuned kernels.  Roles key-disjoint (fresh inserts, Zipf
+    upsert-ADD of live keys, erases, present / absent queries), so every
+    status, value and the final map equal the oracle's sequential replay."""
+    from paper_2509_16407_b200.tables import OP_ERASE, OP_QUERY, OP_UPSERT
+    from paper_2509_16407_b200.workload import zipf_ranks
+    cap = 1 << 19
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * (1 << 16), seed=21)
+    t = _table(cfg)
+    o = _oracle(cfg)
+    base = _keys(41, int(t.capacity_slots * 0.55))
+    t.upsert_batch(_cuda(base), _cuda(base & np.uint64(0xFFFF)))
+    o.upsert_batch(base, base & np.uint64(0xFFFF))
+    nq = 30_000
+    fresh = _keys(42, nq)
+    live = base[4 * nq:]
+    zipf = live[zipf_ranks(len(live), nq, 0.99, seed=3) - 1]
+    ops = np.concatenate([np.full(nq, OP_UPSERT | (2 << 4)), np.full(nq, OP_UPSERT | (2 << 4)),
+                          np.full(nq, OP_ERASE), np.full(nq, OP_QUERY), np.full(nq, OP_QUERY)]).astype(np.uint8)
+    keys = np.concatenate([fresh, zipf, base[:nq], base[nq:2 * nq], _keys(43, nq)])
+    vals = (np.arange(len(keys), dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)
+    perm = np.random.default_rng(7).permutation(len(keys))
+    ops, keys, vals = ops[perm], keys[perm], vals[perm]
+    st, vo = t.mixed_batch(_cuda(ops), _cuda(keys), _cuda(vals), combine=combine, concurrent=True)
+    ost, ovo = o.mixed_batch(ops, keys, vals)
+    bad = np.nonzero((_np(st) != ost) | (_np(vo) != ovo))[0]
+    assert bad.size == 0, [(int(ops[i]), int(_np(st)[i]), int(ost[i])) for i in bad[:10]]
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
+
+
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "p2", "cuckoo", "chaining", "double_md"])
+def test_concurrent_kinds_same_key_races(design):
+    """Concurrent segments where the SAME keys are upserted, erased and
+    queried in one batch (no fixed order): whatever the interleaving, no key
+    is stored twice, keys that were only upserted are present, keys that were
+    only erased (present before) are absent, and every erase that reports
+    success removed a key that existed."""
+    from paper_2509_16407_b200.tables import OP_ERASE, OP_QUERY, OP_UPSERT
+    cap = 1 << 19
+    cfg = cfg_for(design, cap if design != "chaining" else 7 * (1 << 16), seed=22)
+    t = _table(cfg)
+    base = _keys(51, int(t.capacity_slots * 0.5))
+    t.upsert_batch(_cuda(base), _cuda(base))
+    hot = np.concatenate([base[:20_000], _keys(52, 20_000)])   # half present before, half new
+    only_up = _keys(53, 20_000)
+    only_er = base[20_000:40_000]
+    rng = np.random.default_rng(9)
+    k_race = hot[rng.integers(0, len(hot), 60_000)]
+    ops = np.concatenate([rng.choice(np.array([OP_UPSERT, OP_ERASE, OP_QUERY], np.uint8), 60_000),
+                          np.full(20_000, OP_UPSERT), np.full(20_000, OP_ERASE)]).astype(np.uint8)
+    keys = np.concatenate([k_race, only_up, only_er])
+    perm = rng.permutation(len(keys))
+    ops, keys = ops[perm], keys[perm]
+    st, _vo = t.mixed_batch(_cuda(ops), _cuda(keys), _cuda(keys), concurrent=True)
+    st = _np(st)
+    assert t.duplicate_scan() == {}
+    present = dict(t.items())
+    assert all(int(k) in present for k in only_up)
+    assert not any(int(k) in present for k in only_er)
+    er_ok = keys[(ops == OP_ERASE) & (st == 1)]
+    existed = set(base.tolist()) | set(keys[ops == OP_UPSERT].tolist())
+    assert all(int(k) in existed for k in er_ok)
