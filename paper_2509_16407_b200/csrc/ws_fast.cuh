@@ -710,4 +710,193 @@ __global__ void __launch_bounds__(256, MINB) k_upsert_p2md_rounds(Dev d, const u
   }
 }
 
+// Mixed batches in ONE launch (the paper's single-kernel aging; interleaved
+// batches, small mixed batches): k_upsert_p2md_rounds extended with erase and
+// query lanes.  Every lane runs its own op kind in the same warp-synchronous
+// rounds, so the pair-cooperative tag fetches stay warp-collective:
+//   * upsert lanes: exactly the upsert kernel's lock rounds (b0, then b1 when
+//     the shortcut does not apply), per-op merge from the op byte;
+//   * erase lanes (reference openaddr.py:449-473): lock b0 only, find in b0,
+//     else (no early exit) in b1, then the tombstone protocol of
+//     Ctx::tombstone (tombstones_ever, fence, cell := TOMB, fence, tag := 0),
+//     one fence per step for the warp;
+//   * query lanes: lock-free (openaddr.py:433-447), done in the first round.
+// Op bytes whose kind is not upsert / erase run as queries and merges above
+// MIN as REPLACE, as Ctx::run / apply_merge do.  conc_erase 2: the launch's
+// erase count (k_count_erases) decides whether the tombstone flag must be
+// re-read behind a fence.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_mixed_p2md_rounds(Dev d, const u8* __restrict__ ops, u8 uop,
+                                                           const u64* __restrict__ keys,
+                                                           const u64* __restrict__ vals, u64 n, u8* status,
+                                                           u64* vout, int conc_erase, int gated) {
+  WS_PROLOGUE(d, gated, n);
+  const u32 te0 = ld_u32_relaxed(d.state);
+  const bool conc = conc_erase == 2 ? ld_u32_relaxed(d.cs + 3) != 0 : conc_erase != 0;
+  const int lane = threadIdx.x & 31;
+  const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u64 c0 = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5;
+  for (u64 c = c0; c * 32 < n; c += nwarps) {
+    const u64 i = c * 32 + lane;
+    bool pending = i < n;
+    int kind = OP_QUERY, merge = 0;
+    u64 key = 0, val = 0, b0 = 0, b1 = 0;
+    u16 tag = 1;
+    if (pending) {
+      const u8 op = ops ? __ldg(ops + i) : uop;
+      kind = op & 15;
+      if (kind > OP_QUERY) kind = OP_QUERY;
+      merge = op >> 4;
+      key = __ldg(keys + i);
+      val = vals ? __ldg(vals + i) : 0ull;
+      const u64 h0 = mix64(key ^ d.seeds[0]);
+      b0 = d.nbm(h0 >> 16);
+      const u16 t = (u16)(h0 & 0xFFFF);
+      tag = t ? t : (u16)1;
+      b1 = d.nbm(mix64(key ^ d.seeds[1]) >> 16);
+    }
+    const bool locker = kind != OP_QUERY;
+    u8 st = 0;
+    u64 qv = 0;
+    unsigned backoff = 64;
+    // lock discipline of k_upsert_p2md_rounds (ascending waits only); erase
+    // lanes only ever hold b0
+    bool held0 = false, held1 = false, lofirst = false;
+    while (__any_sync(0xFFFFFFFFu, pending)) {
+      if (pending && locker) {
+        if (lofirst) {
+          if (!held1) held1 = try_lock_bucket(d.locks, b1);
+          if (held1 && !held0) held0 = try_lock_bucket(d.locks, b0);
+        } else if (!held0) {
+          held0 = try_lock_bucket(d.locks, b0);
+        }
+      }
+      const bool hold0 = pending && (!locker || held0);
+      bool drop0 = false;
+      u32 M0, Z0;
+      coop_masks<false, true>(d, hold0, b0, tag, M0, Z0);
+      bool hold1 = false, need1 = false, decided = false, te_last = true;
+      i64 del = -1;
+      u64 old;
+      int used0 = 0;
+      if (hold0) {
+        const int j = M0 ? pair_confirm<false, true>(d, b0, M0, key, old) : -1;
+        if (j >= 0) {
+          if (kind == OP_UPSERT) {
+            st_cell(d.cells + 2 * (b0 * 32 + j), key, apply_merge(merge, old, val));
+            st = S_UPDATED;
+            pending = false;
+          } else if (kind == OP_ERASE) {
+            del = (i64)(b0 * 32 + j);
+          } else {
+            st = 1;
+            qv = old;
+            pending = false;
+          }
+        } else {
+          bool te = te0 != 0;
+          if (conc) { fence_acq_rel(); te = ld_u32_relaxed(d.state) != 0; }
+          te_last = te;
+          const int zc0 = __popc(Z0);
+          used0 = 32 - (zc0 < d.zcc ? zc0 : d.zcc);
+          if (kind == OP_UPSERT) {
+            if ((te || used0 >= d.shortcut) && b1 != b0) {
+              if (held1) {
+                hold1 = true;
+              } else {
+                held1 = try_lock_bucket(d.locks, b1);
+                hold1 = held1;
+                if (!held1 && b1 < b0) {
+                  lofirst = true;
+                  drop0 = true;
+                }
+              }
+              need1 = hold1;
+            } else {
+              decided = true;
+            }
+          } else if (!(Z0 && !te && used0 < d.shortcut) && b1 != b0) {
+            need1 = true;  // erase / query: the key may live in the alternate
+          } else {
+            st = 0;  // early exit: provably absent
+            pending = false;
+          }
+        }
+      }
+      u32 M1 = 0, Z1 = 0;
+      if (__any_sync(0xFFFFFFFFu, need1)) coop_masks<false, true>(d, need1, b1, tag, M1, Z1);
+      u64 target = b0;
+      u32 Zt = Z0;
+      if (need1) {
+        const int j = M1 ? pair_confirm<false, true>(d, b1, M1, key, old) : -1;
+        if (kind == OP_UPSERT) {
+          if (j >= 0) {
+            st_cell(d.cells + 2 * (b1 * 32 + j), key, apply_merge(merge, old, val));
+            st = S_UPDATED;
+            pending = false;
+          } else {
+            const int zc1 = __popc(Z1);
+            const int used1 = 32 - (zc1 < d.zcc ? zc1 : d.zcc);
+            const bool prim = used0 <= used1;  // ties go to the primary
+            target = prim ? b0 : b1;
+            Zt = prim ? Z0 : Z1;
+            if (!Zt) { target = prim ? b1 : b0; Zt = prim ? Z1 : Z0; }
+            decided = true;
+          }
+        } else if (kind == OP_ERASE) {
+          if (j >= 0) del = (i64)(b1 * 32 + j);
+          else { st = 0; pending = false; }
+        } else {
+          if (j >= 0) { st = 1; qv = old; }
+          pending = false;
+        }
+      }
+      if (decided) {
+        if (!Zt) {
+          st = S_FULL;
+          pending = false;
+        } else {
+          const u64 slot = target * 32 + (__ffs(Zt) - 1);
+          if (conc) fence_acq_rel();
+          if (!te_last && ((Zt >> ((slot & 31) ^ 1)) & 1u)) st_cell(d.cells + 2 * (slot ^ 1), 0, 0);
+          st_cell(d.cells + 2 * slot, key, val);
+          st_tag(d.tags + slot, tag);
+          st = S_INSERTED;
+          pending = false;
+        }
+      }
+      // tombstones (one fence per step for the warp)
+      if (__any_sync(0xFFFFFFFFu, del >= 0)) {
+        if (del >= 0 && ld_u32_relaxed(d.state) == 0) st_u32_relaxed(d.state, 1u);
+        fence_acq_rel();
+        if (del >= 0) st_cell(d.cells + 2 * (u64)del, TOMB, 0);
+        fence_acq_rel();  // the tombstone is visible before the zero tag that advertises it
+        if (del >= 0) {
+          st_tag(d.tags + (u64)del, 0);
+          st = 1;
+          pending = false;
+        }
+      }
+      __syncwarp();
+      fence_acq_rel();
+      if (held1 && !pending) {
+        red_and_relaxed(d.locks + (b1 >> 5), ~(1u << (b1 & 31)));
+        held1 = false;
+      }
+      if (held0 && (!pending || drop0)) {
+        red_and_relaxed(d.locks + (b0 >> 5), ~(1u << (b0 & 31)));
+        held0 = false;
+      }
+      if (pending) {
+        __nanosleep(backoff + 8 * lane);
+        if (backoff < 4096) backoff <<= 1;
+      }
+    }
+    if (i < n) {
+      if (status) status[i] = st;
+      if (vout) vout[i] = kind == OP_QUERY && st ? qv : 0;
+    }
+  }
+}
+
 }  // namespace ws
