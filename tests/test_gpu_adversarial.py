@@ -18,10 +18,23 @@ def test_safe_designs_zero_duplicates_heavy_delays(design):
     assert rep["duplicate_buckets"] == 0, rep
 
 
-def test_safe_p2md_large_no_delay():
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md", "double_md", "cuckoo"])
+def test_safe_large_no_delay(design):
+    """Without delay injection the interleaved actors run through the tuned
+    single-launch mixed kernels (k_mixed_p2md_rounds, k_mixed_icemd_rounds)
+    where they exist: still no duplicate."""
     from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
-    rep = run_adversarial("p2_md", buckets=200_000, trials=5, seed=11, profile=DelayProfile.off())
+    rep = run_adversarial(design, buckets=200_000, trials=5, seed=11, profile=DelayProfile.off())
     assert rep["duplicate_buckets"] == 0, rep
+
+
+@pytest.mark.parametrize("design", ["p2_md", "iceberg_md"])
+def test_spec_scale_hundred_trials_fused_kernels(design):
+    """SPEC.md:657 scale (>= 100 trials x 10^4 buckets, co-scheduled actors)
+    through the fused mixed kernels (no delays): 0 duplicates."""
+    from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
+    rep = run_adversarial(design, buckets=10_000, trials=100, seed=13, profile=DelayProfile.off())
+    assert rep["trials"] == 100 and rep["duplicate_buckets"] == 0, rep
 
 
 @pytest.mark.parametrize("design", SAFE)
