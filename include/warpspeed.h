@@ -163,16 +163,19 @@ WS_API int ws_read_range(ws_table *t, uint64_t first_word, uint64_t nwords, uint
 WS_API int ws_info(ws_table *t, ws_info_t *info);
 
 /* performance knobs (no semantic effect) */
-#define WS_TUNE_QUERY_ILP 1 /* P2-MD query kernel: 5 = one thread per op with pair-cooperative tag
-                               fetches (default), 3 = lane-pair tiles, 1/2/4/8 = lookups per thread,
-                               0 = generic kernel */
-#define WS_TUNE_L2_POLICY 2 /* 1: tag loads L2 evict_last, cell loads evict_first; 2: 64-byte L2 fills */
-#define WS_TUNE_UPSERT 3    /* P2-MD upsert: 0 one thread per op, 1 lane-pair tiles,
-                               2 warp-synchronous lock rounds, 3 rounds + 64-byte L2 fills,
+#define WS_TUNE_QUERY_ILP 1 /* query kernel: > 0 = the per-design tuned kernels (P2-MD: one thread per
+                               op with pair-cooperative tag fetches; default 5), 0 = generic kernel
+                               (the round-1 variants 1-4/8 -- several lookups per thread, lane-pair
+                               tiles -- measured slower and were removed; their values now select
+                               the default kernel) */
+#define WS_TUNE_L2_POLICY 2 /* 2: 64-byte L2 fills for tag blocks and cells (default); 0/1: 128-byte fills */
+#define WS_TUNE_UPSERT 3    /* upsert kernel: 0 = generic one thread per op; P2-MD 2 = warp-synchronous
+                               lock rounds, 3 = rounds + 64-byte L2 fills,
                                4 = 3 + full-sector cell writes when the partner cell is EMPTY (default);
+                               1 / 5 (lane-pair tiles, deferred lock release: removed) act as 4;
                                cuckoo: 4 = lock rounds + cooperative 8-lane eviction launch (default),
                                6 = lock rounds + one-thread-per-op eviction launch */
-#define WS_TUNE_OCCUPANCY 4 /* tuned kernels: request >= value CTAs/SM from ptxas (0 = compiler choice) */
+#define WS_TUNE_OCCUPANCY 4 /* retired: forcing 4-8 CTAs/SM measured slower; accepted, no effect */
 /* race-window widening for the adversarial duplicate-key test (reference
  * bench/adversarial.py:40-93 DelayProfile): at the hook stages pre_reserve,
  * pre_publish, pre_tombstone, pre_scan the generic kernels sleep up to
@@ -180,9 +183,8 @@ WS_API int ws_info(ws_table *t, ws_info_t *info);
 #define WS_TUNE_DELAY_NS 5
 #define WS_TUNE_DELAY_P16 6
 #define WS_TUNE_DELAY_SEED 7
-#define WS_TUNE_PREFETCH 10  /* tuned P2-MD upsert / query: prefetch the primary tag block of the op
-                               this lane handles `value` grid-stride iterations ahead into L2
-                               (0 = off, the default: measured slower, profiles/prefetch_r02.log) */
+#define WS_TUNE_PREFETCH 10  /* retired: L2 prefetch of a later op's tag block measured slower
+                               (profiles/prefetch_r02.log); accepted, no effect */
 WS_API int ws_tune(ws_table *t, int knob, int value);
 
 /* hash-sharded multi-GPU routing (device pointers): split a batch into

@@ -1236,8 +1236,6 @@ int ws_create(const ws_config* cfg, int device, ws_table** out) {
   d.tune_qilp = 5;
   d.tune_l2pol = 2;
   d.tune_upsert = 4;
-  d.tune_occ = 0;
-  d.tune_pf = 0;  // measured slower at 2^28 and 2^30 (profiles/prefetch_r02.log)
   d.ck_resume = 0;
 
   auto fail = [&](int code) { ws_destroy(t); return code; };
@@ -1568,9 +1566,8 @@ int ws_tune(ws_table* t, int knob, int value) {
       if (value < 0 || value > 2) return WS_ERR_ARG;
       t->d.tune_l2pol = value;
       return WS_OK;
-    case WS_TUNE_OCCUPANCY:
-      t->d.tune_occ = value;
-      return WS_OK;
+    case WS_TUNE_OCCUPANCY:  // retired in round 2 (every forced occupancy measured slower): accepted, no effect
+      return value < 0 ? WS_ERR_ARG : WS_OK;
     case WS_TUNE_DELAY_NS:
       if (value < 0) return WS_ERR_ARG;
       t->d.delay_ns = (u32)value;
@@ -1582,12 +1579,12 @@ int ws_tune(ws_table* t, int knob, int value) {
     case WS_TUNE_DELAY_SEED:
       t->d.delay_seed = mix64((u64)(unsigned)value);
       return WS_OK;
-    case WS_TUNE_PREFETCH:
-      if (value < 0 || value > 4) return WS_ERR_ARG;
-      t->d.tune_pf = value;
-      return WS_OK;
+    case WS_TUNE_PREFETCH:  // retired in round 2 (L2 prefetch measured slower): accepted, no effect
+      return value < 0 || value > 4 ? WS_ERR_ARG : WS_OK;
     case WS_TUNE_UPSERT:
       if (value < 0 || value > 6) return WS_ERR_ARG;
+      // 1 / 5 (removed P2-MD variants) and 6 outside cuckoo select the default
+      if (value == 1 || value == 5 || (value == 6 && t->cfg.design != D_CUCKOO)) value = 4;
       t->d.tune_upsert = value;
       return WS_OK;
     default: return WS_ERR_ARG;

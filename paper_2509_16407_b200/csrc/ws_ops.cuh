@@ -48,11 +48,10 @@ struct Dev {
   Mod nbm, frontm, backm;
   u64 seeds[8];
   int design, bs, md, shortcut, zcc, probe_cap, ways, depth, phased, lock_elided, line_bytes, wpn;
-  int tune_qilp;   // lookups per thread in the tuned query kernel (1, 2, 4)
-  int tune_l2pol;  // 1: tag loads evict_last, cell loads evict_first
-  int tune_upsert; // P2-MD upsert kernel: 0 generic one-thread-per-op, 1 lane pair, 2/3 rounds
-  int tune_occ;    // minimum resident CTAs per SM requested from ptxas (register cap)
-  int tune_pf;     // tuned P2-MD kernels: L2 prefetch distance in grid-stride iterations (0 = off)
+  int tune_qilp;   // > 0: the per-design tuned query kernels, 0: the generic kernel
+  int tune_l2pol;  // 2: 64-byte L2 fills for tag blocks and cells (default)
+  int tune_upsert; // 4: the per-design tuned upsert kernels (default), 0: generic; P2-MD 2/3 = rounds
+                   // without 64-byte fills / whole-sector writes; cuckoo 6 = serial eviction launch
   // cuckoo: this launch continues ops whose first attempt (the locked scan
   // that found every bucket full) already ran in k_upsert_cuckoo_rounds, so
   // ck_upsert starts at the eviction search (launch-local, never stored)
