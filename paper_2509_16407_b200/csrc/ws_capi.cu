@@ -746,11 +746,26 @@ __device__ __forceinline__ u64 merge_of(int merge, u64 a, u64 b) {
 }
 __device__ __forceinline__ u64 dev_n(u64 n, const u64* dn) { return dn && *dn < n ? *dn : n; }
 
+// one slot of the scratch aggregation table: key, folded value (REPLACE: the
+// group's highest batch index + 1), leader (lowest batch index) and group
+// number share one 32-byte sector, so an op touches one DRAM line
+struct __align__(32) AggSlot {
+  u64 key;
+  u64 val;
+  u32 leader;
+  u32 slot2g;
+  u64 pad;
+};
+__global__ void k_agg_init(AggSlot* tab, u64 cap, u64 ident) {
+  for (u64 h = blockIdx.x * (u64)blockDim.x + threadIdx.x; h < cap; h += (u64)gridDim.x * blockDim.x)
+    tab[h] = AggSlot{0ull, ident, 0xFFFFFFFFu, 0u, 0ull};
+}
+
 // Lanes of a warp holding the same key fold first (__match_any_sync), so a
 // Zipf hot key costs one table atomic per warp instead of one per op.
 __global__ void __launch_bounds__(256) k_agg_insert(const u64* __restrict__ keys, const u64* __restrict__ vals,
                                                     const u32* __restrict__ oidx, u64 n, const u64* dn, int merge,
-                                                    u64* tk, u64* tv, u32* leader, u64 mask, u32* grp) {
+                                                    AggSlot* tab, u64 mask, u32* grp) {
   n = dev_n(n, dn);
   const int lane = threadIdx.x & 31;
   const bool fold = merge == M_ADD || merge == M_MAX || merge == M_MIN;
@@ -783,19 +798,27 @@ __global__ void __launch_bounds__(256) k_agg_insert(const u64* __restrict__ keys
     if (act && lane == last) {
       h = mix64(key ^ 0x9E3779B97F4A7C15ull) & mask;
       while (true) {
-        const u64 cur = *(volatile const u64*)(tk + h);
+        const u64 cur = *(volatile const u64*)&tab[h].key;
         if (cur == key) break;
         if (cur == 0) {
-          const u64 prev = atomicCAS((unsigned long long*)(tk + h), 0ull, (unsigned long long)key);
+          const u64 prev = atomicCAS((unsigned long long*)&tab[h].key, 0ull, (unsigned long long)key);
           if (prev == 0 || prev == key) break;
         }
         h = (h + 1) & mask;
       }
-      atomicMin(leader + h, lo);
-      if (merge == M_ADD) atomicAdd((unsigned long long*)(tv + h), (unsigned long long)v);
-      else if (merge == M_MAX) atomicMax((unsigned long long*)(tv + h), (unsigned long long)v);
-      else if (merge == M_MIN) atomicMin((unsigned long long*)(tv + h), (unsigned long long)v);
-      else if (merge == M_REPLACE) atomicMax((unsigned long long*)(tv + h), (unsigned long long)hi + 1);
+      // key, value and leader share the slot's 32-byte sector: one DRAM line
+      // per op.  The leader and the MAX / MIN / REPLACE values only ever move
+      // one way, so an atomic is issued only when the current value (a plain
+      // read; a stale one only costs an extra atomic) would change: a hot
+      // key's group then takes ~ln(m) of them instead of one per warp
+      AggSlot& e = tab[h];
+      if (*(volatile const u32*)&e.leader > lo) atomicMin(&e.leader, lo);
+      unsigned long long* tv = (unsigned long long*)&e.val;
+      const u64 cur = merge == M_ADD ? 0ull : *(volatile const u64*)&e.val;
+      if (merge == M_ADD) atomicAdd(tv, (unsigned long long)v);
+      else if (merge == M_MAX) { if (cur < v) atomicMax(tv, (unsigned long long)v); }
+      else if (merge == M_MIN) { if (cur > v) atomicMin(tv, (unsigned long long)v); }
+      else if (merge == M_REPLACE) { if (cur < (u64)hi + 1) atomicMax(tv, (unsigned long long)hi + 1); }
     }
     h = __shfl_sync(0xFFFFFFFFu, h, last < 0 ? 0 : last);
     if (act) grp[i] = (u32)h;
@@ -807,8 +830,8 @@ __global__ void __launch_bounds__(256) k_agg_insert(const u64* __restrict__ keys
 // position map (pos), the identity when the segment is in batch order.
 __global__ void __launch_bounds__(256) k_agg_compact(const u64* __restrict__ keys, const u64* __restrict__ vals,
                                                      const u32* __restrict__ oidx, const u32* __restrict__ grp,
-                                                     const u32* leader, const u64* tv, const u32* pos, u64 n,
-                                                     const u64* dn, int merge, u64* gkey, u64* gval, u32* slot2g,
+                                                     AggSlot* tab, const u32* pos, u64 n,
+                                                     const u64* dn, int merge, u64* gkey, u64* gval,
                                                      u64* ng) {
   n = dev_n(n, dn);
   const int lane = threadIdx.x & 31;
@@ -817,7 +840,7 @@ __global__ void __launch_bounds__(256) k_agg_compact(const u64* __restrict__ key
     const u64 i = base + lane;
     const u32 h = i < n ? grp[i] : 0u;
     const u32 bi = i < n ? (oidx ? oidx[i] : (u32)i) : 0u;
-    const bool lead = i < n && leader[h] == bi;
+    const bool lead = i < n && tab[h].leader == bi;
     const u32 m = __ballot_sync(0xFFFFFFFFu, lead);
     if (!m) continue;
     u64 at = 0;
@@ -829,11 +852,11 @@ __global__ void __launch_bounds__(256) k_agg_compact(const u64* __restrict__ key
       u64 v;
       if (merge == M_KEEP) v = __ldg(vals + i);  // the leader is the first write
       else if (merge == M_REPLACE) {
-        const u32 w = (u32)(tv[h] - 1);  // highest batch index of the group
+        const u32 w = (u32)(tab[h].val - 1);  // highest batch index of the group
         v = __ldg(vals + (pos ? pos[w] : w));
-      } else v = tv[h];
+      } else v = tab[h].val;
       gval[g] = v;
-      slot2g[h] = (u32)g;
+      tab[h].slot2g = (u32)g;
     }
   }
 }
@@ -844,14 +867,14 @@ __global__ void k_pos_of(const u32* __restrict__ oidx, u64 n, const u64* dn, u32
     pos[oidx[i]] = (u32)i;
 }
 
-__global__ void k_agg_expand(const u32* grp, const u32* leader, const u32* __restrict__ oidx, const u32* slot2g,
+__global__ void k_agg_expand(const u32* grp, const AggSlot* tab, const u32* __restrict__ oidx,
                              u64 n, const u64* dn, const u8* gst, u8* status) {
   n = dev_n(n, dn);
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
     const u32 h = grp[i];
-    const u8 gs = gst[slot2g[h]];
+    const u8 gs = gst[tab[h].slot2g];
     const u32 bi = oidx ? oidx[i] : (u32)i;
-    status[i] = leader[h] == bi ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
+    status[i] = tab[h].leader == bi ? gs : (gs == S_FULL ? (u8)S_FULL : (u8)S_UPDATED);
   }
 }
 
@@ -876,36 +899,29 @@ int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n
     return p;
   };
   auto release = [&]() { for (void* p : mem) cudaFreeAsync(p, s); };
-  const u64 cap = next_pow2(n + n / 2);  // load <= 2/3; ~24 B/slot, L2-resident up to ~3M ops
+  const u64 cap = next_pow2(n + n / 2);  // load <= 2/3; 32 B/slot, L2-resident up to ~2M ops
   u8* gst = (u8*)alloc(n);
   u64* gkey = (u64*)alloc(8 * n);
   u64* gval = (u64*)alloc(8 * n);
   u64* ng = (u64*)alloc(8);
-  u64* tk = (u64*)alloc(8 * cap);
-  u64* tv = (u64*)alloc(8 * cap);
-  u32* leader = (u32*)alloc(4 * cap);
-  u32* slot2g = (u32*)alloc(4 * cap);
+  AggSlot* tab = (AggSlot*)alloc(sizeof(AggSlot) * cap);
   u32* grp = (u32*)alloc(4 * n);
   u32* pos = (oidx && m == M_REPLACE) ? (u32*)alloc(4 * std::max<u64>(nbatch, 1)) : nullptr;
-  if (!gst || !gkey || !gval || !ng || !tk || !tv || !leader || !slot2g || !grp || (oidx && m == M_REPLACE && !pos)) {
+  if (!gst || !gkey || !gval || !ng || !tab || !grp || (oidx && m == M_REPLACE && !pos)) {
     release();
     return WS_ERR_ALLOC;
   }
-  WS_CK(cudaMemsetAsync(tk, 0, 8 * cap, s));
-  WS_CK(cudaMemsetAsync(tv, m == M_MIN ? 0xFF : 0, 8 * cap, s));  // the merge's identity (REPLACE: no winner)
-  WS_CK(cudaMemsetAsync(leader, 0xFF, 4 * cap, s));
-  WS_CK(cudaMemsetAsync(slot2g, 0, 4 * cap, s));
+  k_agg_init<<<grid_for(cap), kThreads, 0, s>>>(tab, cap, m == M_MIN ? ~0ull : 0ull);  // merge identity
   WS_CK(cudaMemsetAsync(ng, 0, 8, s));
   if (pos) k_pos_of<<<grid_for(n), kThreads, 0, s>>>(oidx, n, dn, pos);
-  k_agg_insert<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, n, dn, m, tk, tv, leader, cap - 1, grp);
-  k_agg_compact<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, grp, leader, tv, pos, n, dn, m, gkey, gval, slot2g,
-                                            ng);
+  k_agg_insert<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, n, dn, m, tab, cap - 1, grp);
+  k_agg_compact<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, grp, tab, pos, n, dn, m, gkey, gval, ng);
   rc = cuda_err(cudaGetLastError());
   CallCtx gcx = cx;
   gcx.dn = ng;  // the group count stays on the device
   if (!rc) rc = run_device_plain(t, nullptr, uop, gkey, gval, n, gst, nullptr, s, inner, false, true, false, gcx);
   if (!rc && status) {
-    k_agg_expand<<<grid_for(n), kThreads, 0, s>>>(grp, leader, oidx, slot2g, n, dn, gst, status);
+    k_agg_expand<<<grid_for(n), kThreads, 0, s>>>(grp, tab, oidx, n, dn, gst, status);
     rc = cuda_err(cudaGetLastError());
   }
   release();
