@@ -333,6 +333,20 @@ class HashTable:
         return bool(self._info().tombstones_ever)
 
     # -------------------------------------------------------- public surface
+    # the reference's per-table hash seeds (tables/openaddr.py, cuckoo.py:
+    # self._s0 / _s1 / _s2 = family.seeds[0..2]), read by its tests
+    @property
+    def _s0(self):
+        return self.family.seeds[0]
+
+    @property
+    def _s1(self):
+        return self.family.seeds[1]
+
+    @property
+    def _s2(self):
+        return self.family.seeds[2]
+
     @property
     def num_buckets(self):
         return self._num_buckets

@@ -44,6 +44,12 @@ def gen_uniform_keys(seed: int, count: int) -> np.ndarray:
     return out
 
 
+def gen_uniform_key_list(seed: int, count: int) -> list:
+    """The same stream as gen_uniform_keys as plain ints, for scalar table
+    calls (reference bench/keys.py:43-45)."""
+    return gen_uniform_keys(seed, count).tolist()
+
+
 def derive_seed(master: int, *parts: int) -> int:
     x = master & U64
     for p in parts:
