@@ -131,7 +131,15 @@ __global__ void __launch_bounds__(256) k_upsert_double_rounds(Dev d, const u64* 
   }
 }
 
+// the fused mixed / erase kernel shared with double_md (ws_d_double_md.cu)
+void launch_mixed_dbl(const OpsArgs& a, bool md);
+bool mixed_dbl_ok(const OpsArgs& a);
+
 static void double_ops(const OpsArgs& a, bool def) {
+  if (def && mixed_dbl_ok(a)) {
+    launch_mixed_dbl(a, false);
+    return;
+  }
   const bool upsert_only = !a.ops && (a.uop & 15) == OP_UPSERT;
   if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && !a.d.phased &&
       a.d.tune_upsert == 4) {
