@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(256) k_erase_icemd_rounds(Dev d, const u64* __
 // Ctx::tombstone with one fence per step for the warp) and lock-free query
 // lanes (openaddr.py:593-610) that finish in the first round.  Op bytes of
 // another kind run as queries, merges above MIN as REPLACE (Ctx::run).
-__global__ void __launch_bounds__(256) k_mixed_icemd_rounds(Dev d, const u8* __restrict__ ops, u8 uop,
+__global__ void __launch_bounds__(256, 4) k_mixed_icemd_rounds(Dev d, const u8* __restrict__ ops, u8 uop,
                                                             const u64* __restrict__ keys,
                                                             const u64* __restrict__ vals, u64 n, u8* status,
                                                             u64* vout, int conc_erase, int gated) {

@@ -21,7 +21,7 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
     g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
-    k_mixed_p2md_rounds<1><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status, a.vout,
+    k_mixed_p2md_rounds<3><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status, a.vout,
                                                           a.conc_erase, a.gated);
     return;
   }
@@ -66,7 +66,7 @@ static void p2_md_preload(bool def) {
   preload_fn(k_query_p2md_coop<true, true, 1>);
   preload_fn(k_upsert_p2md_rounds<true, 1, false, true>);
   preload_fn(k_upsert_p2md_rounds<true, 1, true>);
-  preload_fn(k_mixed_p2md_rounds<1>);
+  preload_fn(k_mixed_p2md_rounds<3>);
 }
 
 Launchers launchers_p2_md() { return Launchers{p2_md_ops, p2_md_query, p2_md_locate, p2_md_preload}; }
