@@ -23,7 +23,7 @@ namespace ws {
 // Lock retries follow the ascending-order rule of the P2-MD kernel: a lane
 // keeps its front lock while it retries the (higher) backyard locks.
 template <bool FILL>
-__global__ void __launch_bounds__(256) k_upsert_icemd_rounds(Dev d, const u64* __restrict__ keys,
+__global__ void __launch_bounds__(256, 4) k_upsert_icemd_rounds(Dev d, const u64* __restrict__ keys,
                                                              const u64* __restrict__ vals, u64 n, int merge,
                                                              u8* status, int conc_erase, int gated) {
   WS_PROLOGUE(d, gated, n);
