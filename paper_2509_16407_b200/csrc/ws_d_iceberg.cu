@@ -166,7 +166,7 @@ static void iceberg_ops(const OpsArgs& a, bool def) {
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * 8), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
     k_upsert_ice_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status, a.conc_erase,
                                                       a.gated);
     return;
@@ -175,6 +175,8 @@ static void iceberg_ops(const OpsArgs& a, bool def) {
 }
 static void iceberg_query(const QueryArgs& a, bool def) {
   if (def && a.d.tune_qilp > 0) {
+    // whole-line scans (86-90 registers, 2 CTAs/SM) measured 3-10% faster
+    // with the default 8 CTAs/SM grid than with kTableGridPerSM
     const unsigned g = grid_for(a.n);
     if (a.ro) k_query_ice_lines<true><<<g, kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);
     else k_query_ice_lines<false><<<g, kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);

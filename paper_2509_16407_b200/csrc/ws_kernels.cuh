@@ -15,6 +15,15 @@ __host__ __device__ constexpr int default_bs(int design) {
   return design == D_DOUBLE ? 8 : design == D_CUCKOO ? 8 : design == D_CHAINING ? 7 : 32;
 }
 
+// Table kernels (one op per thread or lane group, random DRAM accesses,
+// lock rounds) are launched with up to kTableGridPerSM CTAs per SM instead of
+// a few resident waves walking the batch grid-stride: the block scheduler
+// then keeps every SM full to the last op.  Measured on P2-MD (2^28 / 2^30,
+// profiles/grid_size_r02.log): 8 -> 256 CTAs/SM takes the query 11.75 ->
+// 10.29 ms / 54.5 -> 43.6 ms and the insert 25.5 -> 24.2 ms / 101.2 -> 94.8
+// ms; the plateau starts near 96.
+constexpr int kTableGridPerSM = 256;
+
 inline unsigned grid_for(u64 n, int threads = kThreads, int per_sm = 8) {
   u64 g = (n + threads - 1) / threads;
   const u64 cap = (u64)kSMs * per_sm;
@@ -140,7 +149,7 @@ void launch_ops_t(const OpsArgs& a) {
                                                                   a.vout, a.redo, a.probes, a.lock_acc,
                                                                   a.conc_erase, a.gated);
   else
-    k_ops<DES, BS, false><<<a.serial ? 1 : grid_for_table(a.n, a.d.nb), a.serial ? 1 : kThreads, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
+    k_ops<DES, BS, false><<<a.serial ? 1 : grid_for_table(a.n, a.d.nb, kThreads, kTableGridPerSM), a.serial ? 1 : kThreads, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
                                                                 a.vout, a.redo, a.probes, a.lock_acc,
                                                                 a.conc_erase, a.gated, a.rlist, a.rcount);
 }
@@ -148,10 +157,10 @@ void launch_ops_t(const OpsArgs& a) {
 template <int DES, int BS>
 void launch_query_t(const QueryArgs& a) {
   if (a.ro)
-    k_query<DES, BS, true><<<grid_for(a.n), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase,
+    k_query<DES, BS, true><<<grid_for(a.n, kThreads, kTableGridPerSM), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase,
                                                                  a.gated);
   else
-    k_query<DES, BS, false><<<grid_for(a.n), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found,
+    k_query<DES, BS, false><<<grid_for(a.n, kThreads, kTableGridPerSM), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found,
                                                                   a.conc_erase, a.gated);
 }
 

@@ -270,13 +270,38 @@ int main(int argc, char** argv) {
     cudaDeviceSynchronize();
     return 0;
   }
+  if (argc > 2 && argv[2][0] == 'g') {  // independent random reads: resident waves vs a 148x256-CTA grid
+    run<32, 3, 8>(buf, bytes, out, 148 * 8, iters, "nc L2::64B 32B, 8 CTAs/SM x16 it");
+    run<32, 3, 8>(buf, bytes, out, 148 * 256, 1, "nc L2::64B 32B, 148x256 CTAs x1 it");
+    run<32, 3, 2>(buf, bytes, out, 148 * 256, 1, "nc L2::64B 32B, 148x256 CTAs x1 it");
+    run_coop<2, 8>(buf, bytes, out, 148 * 8, iters, "coop 2 lanes, 8 CTAs/SM x16 it");
+    run_coop<2, 8>(buf, bytes, out, 148 * 256, 1, "coop 2 lanes, 148x256 CTAs x1 it");
+    cudaDeviceSynchronize();
+    return 0;
+  }
   if (argc > 2 && argv[2][0] == 'q') {
     const u64 tb = bytes / 9 & ~63ull, ntag = 1ull << (63 - __builtin_clzll(tb / 64));
     const char* cells = buf + ntag * 64;
     const u64 ncell = 1ull << (63 - __builtin_clzll((bytes - ntag * 64) / 16));
-    for (int bps : {4, 8}) {
+    // resident waves walking the work (bps = 4, 8 CTAs per SM, 16 iterations
+    // each) vs a grid of 148 x 256 CTAs of one iteration each, the launch
+    // shape of the table kernels (ws_kernels.cuh kTableGridPerSM)
+    for (int bps : {4, 8, -256}) {
       cudaEvent_t a, b;
       cudaEventCreate(&a); cudaEventCreate(&b);
+      if (bps < 0) {
+        const int nb_ = 148 * -bps;
+        chain<2><<<nb_, 256>>>(buf, ntag, cells, ncell, 1, out, 1);
+        cudaEventRecord(a);
+        for (int rep = 0; rep < 16; rep++) chain<2><<<nb_, 256>>>(buf, ntag, cells, ncell, 7 + rep, out, 1);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        const double ch = (double)nb_ * 256 * 2 * 16;
+        printf("chain tags %6llu MiB + cells %6llu MiB, grid 148x256 CTAs: %6.2f G chains/s = %6.2f G acc/s\n",
+               ntag * 64 >> 20, ncell * 16 >> 20, ch / ms / 1e6, 2 * ch / ms / 1e6);
+        continue;
+      }
       chain<2><<<148 * bps, 256>>>(buf, ntag, cells, ncell, 1, out, 1);
       cudaEventRecord(a);
       chain<2><<<148 * bps, 256>>>(buf, ntag, cells, ncell, 7, out, iters);

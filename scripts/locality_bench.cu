@@ -53,9 +53,11 @@ __global__ void __launch_bounds__(256) pairs(char* buf, u64 nlines, long long of
   if (acc == 0x123456789ull) out[0] = acc;
 }
 
+// blocks x iters: 148*8 CTAs walking 16 iterations (round 1) or 148*256 CTAs
+// of one iteration (the launch shape of the table kernels since round 2)
 template <int MODE>
-static float run(char* buf, u64 nlines, long long off, u64* out) {
-  const int R = 4, iters = 16, blocks = 148 * 8;
+static float run(char* buf, u64 nlines, long long off, u64* out, int blocks = 148 * 8, int iters = 16) {
+  const int R = 4;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -86,6 +88,11 @@ int main() {
              cudaGetErrorString(cudaGetLastError()));
       fflush(stdout);
     }
+  for (int mode = 0; mode < 2; mode++) {
+    const float g = mode == 0 ? run<0>(buf, nlines, -1, out, 148 * 256, 1) : run<1>(buf, nlines, -1, out, 148 * 256, 1);
+    printf("mode %d (%s) off     -1, grid 148x256 CTAs x 1 iteration: %.2f G ops/s [%s]\n", mode,
+           mode ? "read+2 stores" : "read+read", g, cudaGetErrorString(cudaGetLastError()));
+  }
   printf("err: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
