@@ -30,7 +30,7 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
     g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
-#define WS_UR(F, PH, FI) k_upsert_p2md_rounds<F, 1, PH, FI><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, \
+#define WS_UR(F, PH, FI) k_upsert_p2md_rounds<F, 4, PH, FI><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, \
                                                    a.n, a.uop >> 4, a.status, a.conc_erase, a.gated)
     if (a.d.phased) { if (a.d.tune_upsert >= 3) WS_UR(true, true, false); else WS_UR(false, true, false); }
     else if (a.d.tune_upsert >= 4) WS_UR(true, false, true);
@@ -49,7 +49,7 @@ static void p2_md_query(const QueryArgs& a, bool def) {
   // one thread per op, pair-cooperative tag fetches
   u64 g = (a.n + 255) / 256;
   g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * kTableGridPerSM);
-#define WS_QC(RO, F) k_query_p2md_coop<RO, F, 1><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, \
+#define WS_QC(RO, F) k_query_p2md_coop<RO, F, 5><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, \
                                                                               a.conc_erase, a.gated)
   const bool f64 = a.d.tune_l2pol == 2;
   if (a.ro) { if (f64) WS_QC(true, true); else WS_QC(true, false); }
@@ -62,10 +62,10 @@ static void p2_md_locate(const LocateArgs& a, bool def) {
 static void p2_md_preload(bool def) {
   if (!def) { preload_t<D_P2_MD, 0>(); return; }
   preload_t<D_P2_MD, 32>();
-  preload_fn(k_query_p2md_coop<false, true, 1>);
-  preload_fn(k_query_p2md_coop<true, true, 1>);
-  preload_fn(k_upsert_p2md_rounds<true, 1, false, true>);
-  preload_fn(k_upsert_p2md_rounds<true, 1, true>);
+  preload_fn(k_query_p2md_coop<false, true, 5>);
+  preload_fn(k_query_p2md_coop<true, true, 5>);
+  preload_fn(k_upsert_p2md_rounds<true, 4, false, true>);
+  preload_fn(k_upsert_p2md_rounds<true, 4, true>);
   preload_fn(k_mixed_p2md_rounds<3>);
 }
 
