@@ -118,7 +118,7 @@ __device__ __forceinline__ void ck_release(const Dev& d, const u64 (&srt)[W], in
 // lanes holding all their locks scan with 32-byte loads, then the warp issues
 // one fence and the finished lanes release with relaxed reductions.
 template <int W>
-__global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* __restrict__ keys, u64 n,
+__global__ void __launch_bounds__(256, 5) k_query_cuckoo_rounds(Dev d, const u64* __restrict__ keys, u64 n,
                                                              u64* vout, u8* found, int gated) {
   WS_PROLOGUE(d, gated, n);
   const int lane = threadIdx.x & 31;
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) k_query_cuckoo_rounds(Dev d, const u64* _
 // bucket's first EMPTY) receives the key.  Ops whose buckets are all full
 // are marked S_RETRY and left to the generic kernel (BFS eviction chains),
 // launched right after on the same stream: one serial order of the batch.
-__global__ void __launch_bounds__(256) k_upsert_cuckoo_rounds(Dev d, const u64* __restrict__ keys,
+__global__ void __launch_bounds__(256, 6) k_upsert_cuckoo_rounds(Dev d, const u64* __restrict__ keys,
                                                               const u64* __restrict__ vals, u64 n, int merge,
                                                               u8* st_out, int gated) {
   WS_PROLOGUE(d, gated, n);
@@ -281,7 +281,7 @@ __device__ __forceinline__ bool line8_has_free(const u64* line) {
   return f;
 }
 
-__global__ void __launch_bounds__(256) k_ck_evict_coop(Dev d, const u64* __restrict__ keys,
+__global__ void __launch_bounds__(256, 5) k_ck_evict_coop(Dev d, const u64* __restrict__ keys,
                                                        const u64* __restrict__ vals, int merge, u8* status,
                                                        const u32* __restrict__ rlist, const u32* rcount,
                                                        int conc_erase) {

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) k_query_double_lines(Dev d, const u64* __
 // into a match, else publishes into the first reusable cell it passed by CAS
 // (writers into a foreign bucket do not hold its lock, sync.py's reserve
 // protocol); a lost CAS re-walks next round.  One fence per warp-round.
-__global__ void __launch_bounds__(256) k_upsert_double_rounds(Dev d, const u64* __restrict__ keys,
+__global__ void __launch_bounds__(256, 4) k_upsert_double_rounds(Dev d, const u64* __restrict__ keys,
                                                               const u64* __restrict__ vals, u64 n, int merge,
                                                               u8* status, int gated) {
   WS_PROLOGUE(d, gated, n);

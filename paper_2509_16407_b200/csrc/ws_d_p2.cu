@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) k_query_p2_lines(Dev d, const u64* __rest
 // publication under the bucket lock, one fence per warp-round, and the same
 // ascending-order retry rule (keep b0 while retrying b1 > b0; release b0 and
 // take b1 first when b1 < b0).
-__global__ void __launch_bounds__(256) k_upsert_p2_rounds(Dev d, const u64* __restrict__ keys,
+__global__ void __launch_bounds__(256, 3) k_upsert_p2_rounds(Dev d, const u64* __restrict__ keys,
                                                           const u64* __restrict__ vals, u64 n, int merge,
                                                           u8* status, int conc_erase, int gated) {
   WS_PROLOGUE(d, gated, n);
