@@ -577,7 +577,7 @@ int run_device_split(ws_table* t, const u8* ops, const u64* keys, const u64* val
     if (ev_q) cudaStreamWaitEvent(s, ev_q, 0);
   }
   if (!rc) {
-    dim3 g(grid_for(n), 3);
+    dim3 g(grid_for(n, kThreads, kTableGridPerSM), 3);
     k_kind_unsplit<<<g, kThreads, 0, s>>>(cnt, o.ie, ste, o.iq, stq, voq, o.ir, str, vor, o.opr, status, vout);
     rc = cuda_err(cudaGetLastError());
   }
@@ -914,14 +914,16 @@ int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n
   k_agg_init<<<grid_for(cap), kThreads, 0, s>>>(tab, cap, m == M_MIN ? ~0ull : 0ull);  // merge identity
   WS_CK(cudaMemsetAsync(ng, 0, 8, s));
   if (pos) k_pos_of<<<grid_for(n), kThreads, 0, s>>>(oidx, n, dn, pos);
-  k_agg_insert<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, n, dn, m, tab, cap - 1, grp);
-  k_agg_compact<<<grid_for(n), 256, 0, s>>>(keys, vals, oidx, grp, tab, pos, n, dn, m, gkey, gval, ng);
+  // random table accesses: the table kernels' launch shape (ws_kernels.cuh kTableGridPerSM)
+  k_agg_insert<<<grid_for(n, 256, kTableGridPerSM), 256, 0, s>>>(keys, vals, oidx, n, dn, m, tab, cap - 1, grp);
+  k_agg_compact<<<grid_for(n, 256, kTableGridPerSM), 256, 0, s>>>(keys, vals, oidx, grp, tab, pos, n, dn, m, gkey,
+                                                                   gval, ng);
   rc = cuda_err(cudaGetLastError());
   CallCtx gcx = cx;
   gcx.dn = ng;  // the group count stays on the device
   if (!rc) rc = run_device_plain(t, nullptr, uop, gkey, gval, n, gst, nullptr, s, inner, false, true, false, gcx);
   if (!rc && status) {
-    k_agg_expand<<<grid_for(n), kThreads, 0, s>>>(grp, tab, oidx, n, dn, gst, status);
+    k_agg_expand<<<grid_for(n, kThreads, kTableGridPerSM), kThreads, 0, s>>>(grp, tab, oidx, n, dn, gst, status);
     rc = cuda_err(cudaGetLastError());
   }
   release();
