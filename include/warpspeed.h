@@ -185,7 +185,13 @@ WS_API int ws_info(ws_table *t, ws_info_t *info);
 #define WS_TUNE_DELAY_SEED 7
 #define WS_TUNE_PREFETCH 10  /* retired: L2 prefetch of a later op's tag block measured slower
                                (profiles/prefetch_r02.log); accepted, no effect */
+#define WS_TUNE_KERNEL_EVENTS 11 /* 1: bracket every table-kernel launch with CUDA events on its stream
+                                    (benchmark instrumentation; read with ws_kernel_times) */
 WS_API int ws_tune(ws_table *t, int knob, int value);
+/* elapsed ms of each table-kernel launch recorded since the last call (in
+ * launch order; waits for them), *count = how many; clears the record.
+ * Benchmark instrumentation for the kernel-level roofline (bench.py). */
+WS_API int ws_kernel_times(ws_table *t, float *ms_out, uint64_t cap, uint64_t *count);
 
 /* hash-sharded multi-GPU routing (device pointers): split a batch into
  * 2^log2_parts per-owner contiguous segments, owner = top log2_parts bits of

@@ -32,12 +32,14 @@ WS_F_CONCURRENT_KINDS = 32
 EXPORTS = ("ws_create", "ws_destroy", "ws_clear", "ws_upsert", "ws_query", "ws_erase", "ws_mixed",
            "ws_locate", "ws_probe_counts", "ws_occupied", "ws_export_items",
            "ws_duplicate_scan", "ws_checksum", "ws_export_raw", "ws_read_range", "ws_info", "ws_tune",
+           "ws_kernel_times",
            "ws_partition", "ws_unpermute", "ws_xchg_create", "ws_xchg_handle", "ws_xchg_open",
            "ws_xchg_run", "ws_xchg_destroy", "ws_strerror")
 WS_TUNE_QUERY_ILP = 1
 WS_TUNE_L2_POLICY = 2
 WS_TUNE_UPSERT = 3
 WS_TUNE_OCCUPANCY = 4
+WS_TUNE_KERNEL_EVENTS = 11
 WS_TUNE_DELAY_NS = 5
 WS_TUNE_DELAY_P16 = 6
 WS_TUNE_DELAY_SEED = 7
@@ -99,6 +101,7 @@ def load():
         lib.ws_read_range.argtypes = [vp, u64, u64, vp, u64, u64, vp, vp]
         lib.ws_info.argtypes = [vp, C.POINTER(WsInfo)]
         lib.ws_tune.argtypes = [vp, i32, i32]
+        lib.ws_kernel_times.argtypes = [vp, vp, u64, C.POINTER(u64)]
         lib.ws_partition.argtypes = [vp, vp, vp, u64, u64, i32, vp, vp, vp, vp, vp, vp]
         lib.ws_unpermute.argtypes = [vp, vp, u64, i32, vp, vp]
         lib.ws_xchg_create.argtypes = [i32, i32, u64, i32, C.POINTER(vp)]

@@ -170,6 +170,12 @@ struct ws_table {
   bool def_bs;
   u64 cell_words;
   u64 lock_words;
+  // WS_TUNE_KERNEL_EVENTS: CUDA events bracket every table-kernel launch of
+  // run_device_plain on its stream (bench.py's per-kernel roofline timing);
+  // ws_kernel_times() reads and clears them
+  bool time_kernels = false;
+  std::mutex ev_mu;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
   // Concurrent calls (reference tables/base.py:5-7: every public op may be
   // called from many threads) hold `mu` shared for their whole host-side
   // duration; only a chaining pool growth (which moves the node arena) takes
@@ -657,6 +663,23 @@ int run_device_by_kind(ws_table* t, const u8* ops, u8 uop, const u64* keys, cons
   return rc;
 }
 
+// open / close a kernel-timing bracket (WS_TUNE_KERNEL_EVENTS)
+cudaEvent_t kev_begin(ws_table* t, cudaStream_t s) {
+  if (!t->time_kernels) return nullptr;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  cudaEventRecord(e, s);
+  return e;
+}
+void kev_end(ws_table* t, cudaStream_t s, cudaEvent_t b) {
+  if (!b) return;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) { cudaEventDestroy(b); return; }
+  cudaEventRecord(e, s);
+  std::lock_guard<std::mutex> g(t->ev_mu);
+  t->kev.push_back({b, e});
+}
+
 int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const u64* vals, u64 n,
                      u8* status, u64* vout, cudaStream_t s, u32 flags, bool has_erase, bool has_upsert,
                      bool query_only, const CallCtx& cx) {
@@ -677,7 +700,9 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
   }
   if (query_only && !(flags & WS_F_SERIAL)) {
     QueryArgs qa{dev_of(t, cx), keys, n, vout, status, conc, gated, t->cfg.phased ? 1 : 0, s};
+    cudaEvent_t kb = kev_begin(t, s);
     t->L.query(qa, t->def_bs);
+    kev_end(t, s, kb);
     return cuda_err(cudaGetLastError());
   }
   const bool chain_up = t->cfg.design == D_CHAINING && has_upsert;
@@ -688,7 +713,9 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
   if (chain_up) WS_CK(cudaMemsetAsync(cx.cs + 2, 0, sizeof(u32), s));
   OpsArgs lo{dev_of(t, cx), ops, uop, keys, vals, n, st, vout, nullptr, nullptr, nullptr, conc, gated, 0,
              (flags & WS_F_SERIAL) ? 1 : 0, s};
+  cudaEvent_t kb = kev_begin(t, s);
   t->L.ops(lo, t->def_bs);
+  kev_end(t, s, kb);
   rc = cuda_err(cudaGetLastError());
   while (rc == WS_OK && chain_up) {
     u64* hp = pin();
@@ -1599,6 +1626,9 @@ int ws_tune(ws_table* t, int knob, int value) {
       return WS_OK;
     case WS_TUNE_PREFETCH:  // retired in round 2 (L2 prefetch measured slower): accepted, no effect
       return value < 0 || value > 4 ? WS_ERR_ARG : WS_OK;
+    case WS_TUNE_KERNEL_EVENTS:
+      t->time_kernels = value != 0;
+      return WS_OK;
     case WS_TUNE_UPSERT:
       if (value < 0 || value > 6) return WS_ERR_ARG;
       // 1 / 5 (removed P2-MD variants) and 6 outside cuckoo select the default
@@ -1607,6 +1637,28 @@ int ws_tune(ws_table* t, int knob, int value) {
       return WS_OK;
     default: return WS_ERR_ARG;
   }
+}
+
+int ws_kernel_times(ws_table* t, float* ms_out, uint64_t cap, uint64_t* count) {
+  if (!t || !count) return WS_ERR_ARG;
+  cudaSetDevice(t->device);
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  {
+    std::lock_guard<std::mutex> g(t->ev_mu);
+    ev.swap(t->kev);
+  }
+  *count = ev.size();
+  int rc = WS_OK;
+  for (u64 i = 0; i < ev.size(); i++) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(ev[i].second) != cudaSuccess ||
+        cudaEventElapsedTime(&ms, ev[i].first, ev[i].second) != cudaSuccess)
+      rc = WS_ERR_CUDA;
+    if (ms_out && i < cap) ms_out[i] = ms;
+    cudaEventDestroy(ev[i].first);
+    cudaEventDestroy(ev[i].second);
+  }
+  return rc;
 }
 
 int ws_info(ws_table* t, ws_info_t* info) {

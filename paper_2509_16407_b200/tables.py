@@ -636,6 +636,19 @@ class HashTable:
         if l2_policy is not None:
             self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_L2_POLICY, int(l2_policy)))
 
+    def time_kernels(self, on=True):
+        """Bracket every table-kernel launch with CUDA events on its stream
+        (benchmark instrumentation); kernel_times() returns and clears them."""
+        self._check(self._lib.ws_tune(self._h, _native.WS_TUNE_KERNEL_EVENTS, int(bool(on))))
+
+    def kernel_times(self, cap=1 << 16):
+        """Elapsed ms of each table-kernel launch since the last call, in
+        launch order (waits for them; at most `cap` are returned)."""
+        buf = np.zeros(cap, dtype=np.float32)
+        n = C.c_uint64()
+        self._check(self._lib.ws_kernel_times(self._h, buf.ctypes.data, cap, C.byref(n)))
+        return buf[: min(int(n.value), cap)].tolist()
+
     def set_delays(self, max_ns=0, prob=0.0, seed=0):
         """Device delay injection at the reference's hook stages (race-window
         widening for adversarial tests; generic kernels only)."""

@@ -23,7 +23,7 @@ def _declared():
 def test_header_declares_the_full_abi():
     names = _declared()
     assert "ws_create" in names and "ws_upsert" in names and "ws_query" in names
-    assert len(names) == 25, names
+    assert len(names) == 26, names
 
 
 def test_library_exports_every_declared_symbol():

@@ -175,3 +175,22 @@ def test_host_resident_mixed_batch_matches_oracle(flags):
     np.testing.assert_array_equal(_np(s), os_)
     np.testing.assert_array_equal(_np(v), ov)
     assert t.occupied_count() == o.occupied_count()
+
+
+def test_kernel_event_timing_records_one_bracket_per_table_kernel():
+    """WS_TUNE_KERNEL_EVENTS (bench.py's kernel-level roofline): one
+    positive elapsed time per table-kernel launch, in launch order; off by
+    default and cleared by each read."""
+    t, _o = _pair("p2_md", log2=20)
+    keys = _cuda(_keys(12, 500_000))
+    t.upsert_batch(keys, keys)
+    assert t.kernel_times() == []
+    t.time_kernels(True)
+    t.upsert_batch(keys, keys)
+    t.query_batch(keys)
+    ms = t.kernel_times()
+    assert len(ms) == 2 and all(x > 0 for x in ms)
+    assert t.kernel_times() == []
+    t.time_kernels(False)
+    t.query_batch(keys)
+    assert t.kernel_times() == []
