@@ -44,8 +44,9 @@ def _worker(rank, world, port, outq, exchange="nccl"):
         from paper_2509_16407_b200 import TableConfig
         from paper_2509_16407_b200.sharded import ShardedTable
         from paper_2509_16407_b200.workload import gen_uniform_keys, mix64_np, zipf_ranks
-        st = ShardedTable(TableConfig(design="p2_md", capacity_slots=1 << 20, seed=42), exchange=exchange,
-                          chunk_ops=1 << 16)
+        # 2^19 slots per rank: every rank's 200K keys keep the load at ~0.4
+        st = ShardedTable(TableConfig(design="p2_md", capacity_slots=(1 << 19) * world, seed=42),
+                          exchange=exchange, chunk_ops=1 << 16)
         n = 200_000
         mine = gen_uniform_keys(100 + rank, n)
         s = _np(st.upsert_batch(_cu(mine), _cu(mine & U64(0xFFFF))))
@@ -89,22 +90,23 @@ def _worker(rank, world, port, outq, exchange="nccl"):
         raise
 
 
-@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
-def test_sharded_two_ranks_one_gpu(exchange):
+@pytest.mark.parametrize("world,exchange", [(2, "nccl"), (2, "p2p"), (4, "p2p"), (8, "p2p")])
+def test_sharded_two_ranks_one_gpu(world, exchange):
     """exchange="nccl" runs the all-to-all path (gloo-staged here); "p2p"
-    runs the fused routing kernels over CUDA-IPC peer memory (two processes
-    on one device share it just like NVLink peers), with 2^16-op rounds so
-    the 200K-op batches take several rounds."""
+    runs the fused routing kernels over CUDA-IPC peer memory (processes on
+    one device share it just like NVLink peers), with 2^16-op rounds so the
+    200K-op batches take several rounds.  World 4 and 8 exercise the p2p
+    exchange with as many peers as one 8-GPU node has."""
     ctx = mp.get_context("spawn")
     outq = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, outq, exchange)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, outq, exchange)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(outq.get(timeout=600) for _ in procs)
+    res = dict(outq.get(timeout=900) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: "ok", 1: "ok"}, res
+    assert res == {r: "ok" for r in range(world)}, res
 
 
 def _kmer_worker(rank, world, port, outq, exchange):
