@@ -312,7 +312,13 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
       !(flags & (WS_F_SERIAL | WS_F_INTERLEAVED | kF_NO_KIND_SORT)))
     return run_device_by_kind(t, ops, uop, keys, vals, n, status, vout, s, flags, has_erase, has_upsert, cx);
   const bool sync = (flags & WS_F_SYNC_CHECK) != 0;
-  int rc = validate(keys, ops, n, s, sync, flags, cx);
+  // A query batch mutates nothing, so its sentinel check can ride inside the
+  // query kernel (P2-MD's tuned query counts sentinel keys into this call's
+  // invalid-key word) instead of a separate pass over the keys first; the
+  // verdict is read after the kernel.
+  const bool fuse_check = query_only && n && !(flags & (WS_F_SERIAL | WS_F_NO_CHECK)) && !cx.dn &&
+                          t->cfg.design == D_P2_MD && t->def_bs && t->d.tune_qilp > 0;
+  int rc = fuse_check ? WS_OK : validate(keys, ops, n, s, sync, flags, cx);
   if (rc) return rc;
   if (!n) return WS_OK;
   const int gated = (flags & kF_VALIDATED) ? 1 : (flags & WS_F_NO_CHECK) ? 0 : 1;
@@ -324,11 +330,19 @@ int run_device_plain(ws_table* t, const u8* ops, u8 uop, const u64* keys, const 
     conc = 2;
   }
   if (query_only && !(flags & WS_F_SERIAL)) {
-    QueryArgs qa{dev_of(t, cx), keys, n, vout, status, conc, gated, t->cfg.phased ? 1 : 0, s};
+    QueryArgs qa{dev_of(t, cx), keys, n, vout, status, conc, fuse_check ? 0 : gated, t->cfg.phased ? 1 : 0, s};
+    qa.check_keys = fuse_check ? 1 : 0;
+    if (fuse_check) WS_CK(cudaMemsetAsync(cx.cs, 0, 2 * sizeof(u32), s));
     cudaEvent_t kb = kev_begin(t, s);
     t->L.query(qa, t->def_bs);
     kev_end(t, s, kb);
-    return cuda_err(cudaGetLastError());
+    rc = cuda_err(cudaGetLastError());
+    if (rc || !fuse_check || !sync) return rc;
+    u64* hp = pin();
+    if (!hp) return WS_ERR_ALLOC;
+    WS_CK(cudaMemcpyAsync(hp, cx.cs, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    WS_CK(cudaStreamSynchronize(s));
+    return *(const u32*)hp ? WS_ERR_INVALID_KEY : WS_OK;
   }
   const bool chain_up = t->cfg.design == D_CHAINING && has_upsert;
   u8* st = status;

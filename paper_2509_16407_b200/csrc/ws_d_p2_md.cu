@@ -50,7 +50,7 @@ static void p2_md_query(const QueryArgs& a, bool def) {
   u64 g = (a.n + 255) / 256;
   g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * kTableGridPerSM);
 #define WS_QC(RO, F) k_query_p2md_coop<RO, F, 5><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, \
-                                                                              a.conc_erase, a.gated)
+                                                                              a.conc_erase, a.gated, a.check_keys)
   const bool f64 = a.d.tune_l2pol == 2;
   if (a.ro) { if (f64) WS_QC(true, true); else WS_QC(true, false); }
   else { if (f64) WS_QC(false, true); else WS_QC(false, false); }

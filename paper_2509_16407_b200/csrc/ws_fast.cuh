@@ -113,7 +113,7 @@ __device__ __forceinline__ void coop_masks(const Dev& d, bool active, u64 b, u16
 // One thread per query, pair-cooperative tag fetches (see coop_masks).
 template <bool RO, bool F64, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64* __restrict__ keys, u64 n, u64* vout,
-                                                         u8* found, int conc_erase, int gated) {
+                                                         u8* found, int conc_erase, int gated, int check_keys = 0) {
   WS_PROLOGUE(d, gated, n);
   const u32 te0 = ld_u32_relaxed(d.state);
   const u64 stride = (u64)gridDim.x * blockDim.x;
@@ -123,6 +123,8 @@ __global__ void __launch_bounds__(256, MINB) k_query_p2md_coop(Dev d, const u64*
     const u64 i = base + (threadIdx.x & 31);
     const bool act = i < n;
     const u64 key = act ? __ldg(keys + i) : 0;
+    if (check_keys && __any_sync(0xFFFFFFFFu, act && is_sentinel(key)) && (threadIdx.x & 31) == 0)
+      atomicAdd(d.cs, 1u);  // a sentinel (0, 2^64-2, 2^64-1) among this warp's keys (k_validate's rule)
     const u64 h0 = mix64(key ^ d.seeds[0]);
     const u64 b0 = d.nbm(h0 >> 16);
     const u16 t = (u16)(h0 & 0xFFFF);

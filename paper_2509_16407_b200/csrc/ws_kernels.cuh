@@ -130,6 +130,7 @@ struct QueryArgs {
   u8* found;
   int conc_erase, gated, ro;
   cudaStream_t s;
+  int check_keys = 0;  // count sentinel keys into d.cs[0] (kernels that support it: P2-MD's tuned query)
 };
 
 struct LocateArgs {

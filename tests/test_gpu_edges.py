@@ -194,3 +194,25 @@ def test_kernel_event_timing_records_one_bracket_per_table_kernel():
     t.time_kernels(False)
     t.query_batch(keys)
     assert t.kernel_times() == []
+
+
+@pytest.mark.parametrize("pos", [0, 123_457, 999_999])
+def test_query_sentinel_anywhere_in_large_batch_raises(pos):
+    """The P2-MD query checks sentinels inside the query kernel (no separate
+    pass): a sentinel anywhere in a 10^6-key batch still raises, and the
+    same batch without it answers exactly."""
+    from paper_2509_16407_b200 import InvalidKeyError
+    t, o = _pair("p2_md", log2=20)
+    keys = _keys(13, 500_000)
+    t.upsert_batch(_cuda(keys), _cuda(keys))
+    o.upsert_batch(keys, keys)
+    q = np.concatenate([keys, _keys(14, 500_000)])
+    for bad in (0, (1 << 64) - 1, (1 << 64) - 2):
+        qb = q.copy()
+        qb[pos] = np.uint64(bad)
+        with pytest.raises(InvalidKeyError):
+            t.query_batch(_cuda(qb))
+    f, v = t.query_batch(_cuda(q))
+    of, ov = o.query_batch(q)
+    np.testing.assert_array_equal(_np(f).astype(bool), of.astype(bool))
+    np.testing.assert_array_equal(_np(v), ov)
