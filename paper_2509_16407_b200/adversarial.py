@@ -118,7 +118,7 @@ def actor_layout(xs, ys, warp: int = 32):
 
 
 def run_adversarial(design: str, buckets: int = 10_000, trials: int = 3, seed: int = 5,
-                    profile: DelayProfile | None = None, device=None) -> dict:
+                    profile: DelayProfile | None = None, device=None, keep_table: bool = False) -> dict:
     """`trials` replays over `buckets` primary buckets; returns total duplicate
     buckets and per-trial counts (any duplicate on a synchronised design is a
     correctness failure)."""
@@ -152,6 +152,9 @@ def run_adversarial(design: str, buckets: int = 10_000, trials: int = 3, seed: i
         dups = table.duplicate_scan()
         assert all(k in y_set for k in dups), "duplicate of a non-replayed key"
         per_trial.append(len(dups))
-    return {"design": design, "buckets": buckets, "trials": trials,
-            "replays": buckets * trials, "duplicate_buckets": sum(per_trial),
-            "per_trial": per_trial, "actors_per_bucket": 3}
+    rep = {"design": design, "buckets": buckets, "trials": trials,
+           "replays": buckets * trials, "duplicate_buckets": sum(per_trial),
+           "per_trial": per_trial, "actors_per_bucket": 3}
+    if keep_table:  # the last trial's table, for further inspection
+        rep["table"] = table
+    return rep

@@ -154,6 +154,39 @@ __global__ void k_pair_keys(const ulonglong2* pairs, u64 n, u64* keys) {
 }
 
 // sorted keys -> (key, multiplicity) for every run longer than one
+// duplicate scan for tables too large to sort their keys (see
+// dup_scan_by_locate): the live keys of pair range [lo, lo+m), compacted
+// with their pair indices (warp-aggregated), then compared with where the
+// design's own search finds each key
+__global__ void k_live_keys(Dev d, u64 lo, u64 m, u64 next_node, u64* keys, u64* idx, u64* cnt) {
+  const int lane = threadIdx.x & 31;
+  for (u64 base = (blockIdx.x * (u64)blockDim.x + threadIdx.x) & ~31ull; base < m;
+       base += (u64)gridDim.x * blockDim.x) {
+    const u64 j = base + lane;
+    u64 k = 0, v;
+    const bool live = j < m && pair_live(d, lo + j, next_node, k, v);
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, live);
+    if (!b) continue;
+    u64 at = 0;
+    if (lane == 0) at = atomicAdd((unsigned long long*)cnt, (unsigned long long)__popc(b));
+    at = __shfl_sync(0xFFFFFFFFu, at, 0);
+    if (live) {
+      const u64 p = at + __popc(b & ((1u << lane) - 1));
+      keys[p] = k;
+      idx[p] = lo + j;
+    }
+  }
+}
+__global__ void k_dup_located(const u64* keys, const u64* idx, const i64* loc, const u64* cnt, u64* dk, u64 cap,
+                              u64* ndup) {
+  const u64 m = *cnt;
+  for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < m; i += (u64)gridDim.x * blockDim.x) {
+    if (loc[i] == (i64)idx[i]) continue;  // the search finds this very copy
+    const u64 at = atomicAdd((unsigned long long*)ndup, 1ull);
+    if (at < cap) dk[at] = keys[i];
+  }
+}
+
 __global__ void k_dup_runs(const u64* sorted, u64 n, u64* dk, u64* dc, u64 cap, u64* ndup) {
   for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i + 1 < n; i += (u64)gridDim.x * blockDim.x) {
     if (sorted[i] != sorted[i + 1] || (i > 0 && sorted[i - 1] == sorted[i])) continue;
@@ -593,6 +626,58 @@ int next_node_of(ws_table* t, cudaStream_t s, u64& nn) {
 }
 
 // live pairs compacted (in slot order) into a fresh device buffer
+// Duplicates of a table too large to sort its keys beside it (2^32 slots:
+// 64 GiB of cells; sorting the live keys needs ~3x their 8 B each): every
+// live copy whose key the design's own search (Ctx::locate, the reference's
+// slot_of) finds at a DIFFERENT slot is an extra copy.  Chunked over the
+// pair array, O(chunk) scratch.  Reports extra copies (a key stored three
+// times counts twice), each listed key with count 2.
+int dup_scan_by_locate(ws_table* t, cudaStream_t s, u64* dup_keys, u64* dup_counts, u64 cap, u64* ndup_out) {
+  u64 nn;
+  int rc = next_node_of(t, s, nn);
+  if (rc) return rc;
+  const u64 np = npairs_of(t), chunk = std::min<u64>(np, (u64)1 << 27);
+  u64 *keys = nullptr, *idx = nullptr, *cnt = nullptr, *dk = nullptr, *nd = nullptr;
+  i64* loc = nullptr;
+  const u64 cap_d = std::max<u64>(cap, 1);
+  WS_CK(cudaMallocAsync((void**)&keys, 8 * chunk, s));
+  WS_CK(cudaMallocAsync((void**)&idx, 8 * chunk, s));
+  WS_CK(cudaMallocAsync((void**)&loc, 8 * chunk, s));
+  WS_CK(cudaMallocAsync((void**)&cnt, 8, s));
+  WS_CK(cudaMallocAsync((void**)&dk, 8 * cap_d, s));
+  WS_CK(cudaMallocAsync((void**)&nd, 8, s));
+  WS_CK(cudaMemsetAsync(nd, 0, 8, s));
+  u64* hp = pin();
+  if (!hp) return WS_ERR_ALLOC;
+  for (u64 lo = 0; lo < np && !rc; lo += chunk) {
+    const u64 m = std::min<u64>(chunk, np - lo);
+    WS_CK(cudaMemsetAsync(cnt, 0, 8, s));
+    k_live_keys<<<grid_for(m), kThreads, 0, s>>>(t->d, lo, m, nn, keys, idx, cnt);
+    WS_CK(cudaMemcpyAsync(hp, cnt, 8, cudaMemcpyDeviceToHost, s));
+    WS_CK(cudaStreamSynchronize(s));
+    const u64 live = hp[0];
+    if (!live) continue;
+    LocateArgs la{t->d, keys, live, loc, s};
+    t->L.locate(la, t->def_bs);
+    k_dup_located<<<grid_for(live), kThreads, 0, s>>>(keys, idx, loc, cnt, dk, cap_d, nd);
+    rc = cuda_err(cudaGetLastError());
+  }
+  if (!rc) rc = cuda_err(cudaMemcpyAsync(hp, nd, 8, cudaMemcpyDeviceToHost, s));
+  if (!rc) rc = cuda_err(cudaStreamSynchronize(s));
+  const u64 ndup = rc ? 0 : hp[0];
+  const u64 mcopy = std::min<u64>(ndup, cap);
+  if (!rc && mcopy && dup_keys) rc = cuda_err(cudaMemcpyAsync(dup_keys, dk, 8 * mcopy, cudaMemcpyDefault, s));
+  if (!rc && mcopy && dup_counts) {
+    std::vector<u64> two(mcopy, 2);
+    rc = cuda_err(cudaMemcpyAsync(dup_counts, two.data(), 8 * mcopy, cudaMemcpyDefault, s));
+    if (!rc) rc = cuda_err(cudaStreamSynchronize(s));
+  }
+  for (void* p : {(void*)keys, (void*)idx, (void*)loc, (void*)cnt, (void*)dk, (void*)nd}) cudaFreeAsync(p, s);
+  if (!rc) rc = cuda_err(cudaStreamSynchronize(s));
+  if (ndup_out) *ndup_out = ndup;
+  return rc;
+}
+
 int compact_items(ws_table* t, cudaStream_t s, ulonglong2** out, u64* count) {
   u64 nn;
   int rc = next_node_of(t, s, nn);
@@ -954,6 +1039,15 @@ int ws_duplicate_scan(ws_table* t, uint64_t* dup_keys, uint64_t* dup_counts, uin
   if (!t) return WS_ERR_ARG;
   cudaSetDevice(t->device);
   cudaStream_t s = S(stream);
+  // the sort below needs the live pairs, their keys twice and the sort's
+  // scratch (~40 B per slot at worst); open-addressing tables too large for
+  // that next to themselves take the chunked search-based scan
+  if (t->cfg.design != D_CHAINING) {
+    size_t fr = 0, tot = 0;
+    const bool force = getenv("WS_DUPSCAN_BY_LOCATE") != nullptr;  // test hook
+    if (force || (cudaMemGetInfo(&fr, &tot) == cudaSuccess && (double)fr < 40.0 * (double)npairs_of(t)))
+      return dup_scan_by_locate(t, s, (u64*)dup_keys, (u64*)dup_counts, cap, (u64*)n_dup_out);
+  }
   ulonglong2* sel = nullptr;
   u64 cnt = 0;
   int rc = compact_items(t, s, &sel, &cnt);

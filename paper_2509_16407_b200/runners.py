@@ -522,6 +522,64 @@ def run_kmer(genome_len: int = 1 << 24, k: int = 31, capacity: int = 1 << 25, de
             "ms": ms, "mops": _mops(len(km), ms), "occupied": t.occupied_count()}
 
 
+def _kmers_device(genome, lo: int, m: int, k: int = 31):
+    """Canonical k-mers (2 bits/base, +1) starting at genome[lo:lo+m] of a
+    device uint8 base tensor -- the device twin of workload.kmer_keys (test
+    workload generation for config 5 at full size, not a table path)."""
+    torch = _torch()
+    fwd = torch.zeros(m, dtype=torch.int64, device=genome.device)
+    rev = torch.zeros(m, dtype=torch.int64, device=genome.device)
+    for j in range(k):
+        b = genome[lo + j:lo + j + m].to(torch.int64)
+        fwd = (fwd << 2) | b
+        rev = rev | ((3 - b) << (2 * j))
+    return (torch.minimum(fwd, rev) + 1).view(torch.uint64)
+
+
+def run_kmer_full(log2_slots: int = 32, load: float = 0.9, repeats: int = 2, k: int = 31, seed: int = 7,
+                  chunk: int = 1 << 27, design: str = "p2_md") -> dict:
+    """BASELINE config 5 at its stated size on one B200 (2^32 P2-MD slots =
+    64 GiB of cells + 8 GiB of tags, SURVEY 8(a) sizing): a seeded random
+    genome of load * 2^32 bases is generated on the device, and its canonical
+    31-mers are upsert-ADDed `repeats` times in chunks of `chunk` k-mers, so
+    the distinct-key load is ~`load` and every k-mer's count is `repeats`
+    times its multiplicity in the genome.  Checked: no FULL, no duplicates,
+    the table's value sum equals repeats x the number of k-mers, every k-mer
+    of the genome is found with a positive multiple of `repeats`."""
+    from .tables import make_table
+    torch = _torch()
+    cap = 1 << log2_slots
+    t = make_table(TableConfig(design=design, capacity_slots=cap, seed=seed))
+    dev = t.device
+    n_kmers = int(cap * load)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    genome = torch.randint(0, 4, (n_kmers + k - 1,), dtype=torch.uint8, device=dev, generator=g)
+    ones = torch.ones(chunk, dtype=torch.int64, device=dev).view(torch.uint64)
+    ms, fulls = 0.0, 0
+    for _rep in range(repeats):
+        for lo in range(0, n_kmers, chunk):
+            m = min(chunk, n_kmers - lo)
+            km = _kmers_device(genome, lo, m, k)
+            with _Timer() as tm:
+                st = t.upsert_batch(km, ones[:m], merge="add", check=False)
+            ms += tm.ms
+            fulls += int((st == 2).sum())
+    occupied, _sk, sv, _x = t.checksum()
+    found_all, mult_ok = True, True
+    for lo in range(0, n_kmers, chunk):
+        m = min(chunk, n_kmers - lo)
+        f, v = t.query_batch(_kmers_device(genome, lo, m, k), check=False)
+        found_all &= bool(f.bool().all())
+        vv = v.view(torch.int64)
+        mult_ok &= bool(((vv > 0) & (vv % repeats == 0)).all())
+    dups = t.duplicate_count()
+    ok = fulls == 0 and dups == 0 and sv == repeats * n_kmers and found_all and mult_ok
+    return {"ok": ok, "slots": cap, "kmers": n_kmers, "repeats": repeats, "upserts": repeats * n_kmers,
+            "distinct": occupied, "load": occupied / cap, "fulls": fulls, "duplicates": dups,
+            "value_sum_exact": sv == repeats * n_kmers, "ms": ms, "mops": _mops(repeats * n_kmers, ms)}
+
+
 YCSB_MIX = {"A": 0.50, "B": 0.05, "C": 0.0}  # update fraction (reference apps/ycsb.py:21)
 
 

@@ -84,3 +84,28 @@ def test_serial_replay_never_races():
                           serial=True)
     assert t.duplicate_scan() == {}
     assert dict(t.items()) == {int(y): 1 for y in ys}
+
+
+@pytest.mark.parametrize("design", ["unsafe_reference", "p2_md", "iceberg_md", "cuckoo", "double"])
+def test_duplicate_scan_by_locate_agrees_with_sort(design):
+    """The chunked search-based duplicate scan (used when a table is too
+    large to sort its keys beside it, e.g. 2^32 slots) agrees with the
+    sort-based one: on the unsafe design's raced table (duplicates stored
+    twice) and on safe tables (none); the test hook WS_DUPSCAN_BY_LOCATE
+    forces the search-based path."""
+    from paper_2509_16407_b200.adversarial import DelayProfile, run_adversarial
+    rep = run_adversarial(design, buckets=20_000, trials=1, seed=5, profile=DelayProfile(0.35, 20_000),
+                          keep_table=True)
+    t = rep["table"]
+    by_sort = t.duplicate_count()
+    import os
+    os.environ["WS_DUPSCAN_BY_LOCATE"] = "1"
+    try:
+        by_locate = t.duplicate_count()
+    finally:
+        del os.environ["WS_DUPSCAN_BY_LOCATE"]
+    assert by_locate == by_sort
+    if design == "unsafe_reference":
+        assert by_sort >= 1
+    else:
+        assert by_sort == 0

@@ -95,3 +95,12 @@ def test_config4_fill_to_095_full_size(design, cap):
     assert f[:npos].all() and not f[npos:].any()
     assert (v[:npos] == (q[:npos] & np.uint64(0xFFFF))).all()
     assert t.duplicate_count() == 0
+
+
+def test_config5_device_kmer_counting():
+    """runners.run_kmer_full (config 5's full-size runner, device-generated
+    genome) at 2^24 slots: no FULL, no duplicates, exact value sum, every
+    k-mer found with a multiple of the repeat count."""
+    from paper_2509_16407_b200 import runners
+    r = runners.run_kmer_full(log2_slots=24, repeats=3, chunk=1 << 22)
+    assert r["ok"], r
