@@ -91,6 +91,18 @@ def main():
         assert (st.cpu().numpy() == ost).all() and (vo.cpu().view(torch.int64).numpy().view(U64) == ovo).all(), d
         assert dict(t.items()) == o.as_dict(), d
         print("ok split+combine", d, flush=True)
+    # the search-based duplicate scan and the query's in-kernel sentinel check
+    import os
+    cfg = cfg_for("p2_md", 1 << 16, seed=8)
+    t = make_table(cfg)
+    k = gen_uniform_keys(25, 50_000)
+    t.upsert_batch(cu(k), cu(k))
+    os.environ["WS_DUPSCAN_BY_LOCATE"] = "1"
+    assert t.duplicate_count() == 0
+    del os.environ["WS_DUPSCAN_BY_LOCATE"]
+    f, _v = t.query_batch(cu(k))
+    assert bool(f.bool().all())
+    print("ok dupscan-by-locate + fused query check", flush=True)
     torch.cuda.synchronize()
     print("sanitize smoke ok", flush=True)
 
