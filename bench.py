@@ -261,6 +261,33 @@ def reference_cpython_rate(load: float, threads: int, log2_slots: int = 18, seed
                       "(bench/runners.py timed_insert / timed_query)"}
 
 
+def reference_cpython_config1(seed: int = 42) -> dict:
+    """BASELINE config 1 ("runs on the CPU reference") on the unmodified
+    reference package at its full size: double hashing, 2^20 slots, 891,289
+    inserts (0.85 load), 2^19 interleaved 50/50 queries, timed with the
+    reference's own timed_insert / timed_query on one thread (~15 s)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "warpbench")):
+        return {"unavailable": "baseline/_ref/warpbench not installed"}
+    if ref not in sys.path:
+        sys.path.append(ref)
+    from warpbench.bench.keys import derive_seed as rderive
+    from warpbench.bench.keys import gen_uniform_keys as rkeys
+    from warpbench.bench.runners import timed_insert, timed_query
+    from warpbench.core import TableConfig as RCfg
+    from warpbench.tables import make_table as rmake
+    t = rmake(RCfg(design="double", capacity_slots=1 << 20, seed=seed))
+    n = int((1 << 20) * 0.85)
+    keys = [int(x) for x in rkeys(seed, n)]
+    miss = [int(x) for x in rkeys(rderive(seed, 0xFEED), 1 << 18)]
+    q = [k for pair in zip(keys[: 1 << 18], miss) for k in pair]
+    dt_i, full = timed_insert(t, keys, 1)
+    dt_q, _ = timed_query(t, q, 1, expect_found=True)
+    return {"workload": "double 2^20 slots: 891,289 inserts (0.85) + 2^19 interleaved 50/50 queries",
+            "insert_mops": round(n / dt_i / 1e6, 4), "query_mops": round(len(q) / dt_q / 1e6, 4),
+            "seconds": round(dt_i + dt_q, 2), "threads": 1, "full": full}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -291,6 +318,7 @@ def run_reference(args, rank, world):
                          "sample": desc},
         # the reference itself (pure Python), BASELINE.md section 3
         "reference_cpython": [reference_cpython_rate(args.load, th) for th in sorted({1, threads})],
+        "reference_cpython_config1": reference_cpython_config1(),
         "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
