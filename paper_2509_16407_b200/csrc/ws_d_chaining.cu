@@ -148,7 +148,7 @@ static void chaining_ops(const OpsArgs& a, bool def) {
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
     k_upsert_chain_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status, a.gated);
     return;
   }
@@ -156,7 +156,7 @@ static void chaining_ops(const OpsArgs& a, bool def) {
 }
 static void chaining_query(const QueryArgs& a, bool def) {
   if (def && !a.conc_erase && a.d.wpn == 16 && a.d.tune_qilp > 0) {
-    const unsigned g = grid_for(a.n, kThreads, kTableGridPerSM);
+    const unsigned g = grid_for(a.n, kThreads, table_grid_per_sm(a.d));
     if (a.ro) k_query_chain_lines<true><<<g, kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);
     else k_query_chain_lines<false><<<g, kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);
     return;

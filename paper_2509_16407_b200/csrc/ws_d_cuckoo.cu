@@ -400,7 +400,7 @@ static void cuckoo_ops(const OpsArgs& a, bool def) {
     if (st) {
       u64 g = (a.n + 255) / 256;
       const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-      g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+      g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
       k_upsert_cuckoo_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, st, a.gated);
       OpsArgs lo = a;
       lo.status = st;
@@ -411,14 +411,14 @@ static void cuckoo_ops(const OpsArgs& a, bool def) {
       u32* rl = nullptr;
       if (a.n < 0xFFFFFFFFull && cudaMallocAsync((void**)&rl, 4 * (a.n + 1), a.s) == cudaSuccess) {
         cudaMemsetAsync(rl + a.n, 0, 4, a.s);
-        k_compact_retry<<<(unsigned)std::max<u64>(std::min<u64>((a.n + 255) / 256, (u64)kSMs * kTableGridPerSM), 1), 256, 0,
+        k_compact_retry<<<(unsigned)std::max<u64>(std::min<u64>((a.n + 255) / 256, (u64)kSMs * table_grid_per_sm(a.d)), 1), 256, 0,
                           a.s>>>(st, a.n, rl, rl + a.n, a.d.dn);
         lo.rlist = rl;
         lo.rcount = rl + a.n;
       }
       if (rl && a.vals && a.d.tune_upsert == 4) {
         // 8 lanes per op; the grid covers the worst case (every op retries)
-        const u64 g = std::max<u64>(std::min<u64>((8 * a.n + 255) / 256, (u64)kSMs * kTableGridPerSM), 1);
+        const u64 g = std::max<u64>(std::min<u64>((8 * a.n + 255) / 256, (u64)kSMs * table_grid_per_sm(a.d)), 1);
         k_ck_evict_coop<<<(unsigned)g, 256, 0, a.s>>>(lo.d, a.keys, a.vals, a.uop >> 4, st, rl, rl + a.n,
                                                       a.conc_erase);
       } else {
@@ -434,7 +434,7 @@ static void cuckoo_ops(const OpsArgs& a, bool def) {
 static void cuckoo_query(const QueryArgs& a, bool def) {
   if (def && a.d.ways <= 8 && a.d.tune_qilp > 0) {
     u64 g = (a.n + 255) / 256;
-    g = std::max<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), 1);
+    g = std::max<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), 1);
     if (a.d.ways == 3)
       k_query_cuckoo_rounds<3><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.gated);
     else

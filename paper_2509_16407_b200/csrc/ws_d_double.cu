@@ -144,7 +144,7 @@ static void double_ops(const OpsArgs& a, bool def) {
   if (def && upsert_only && !a.instr && !a.d.delay_ns && !a.serial && !a.redo && !a.d.phased &&
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
-    g = std::max<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), 1);
+    g = std::max<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), 1);
     k_upsert_double_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status, a.gated);
     return;
   }

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) k_mixed_dbl_rounds(Dev d, const u8* __res
 void launch_mixed_dbl(const OpsArgs& a, bool md) {
   u64 g = (a.n + 255) / 256;
   const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-  g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+  g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
   if (md)
     k_mixed_dbl_rounds<D_DOUBLE_MD, 32><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n,
                                                                       a.status, a.vout, a.conc_erase, a.gated);
@@ -148,7 +148,7 @@ static void double_md_ops(const OpsArgs& a, bool def) {
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
     k_upsert_dblmd_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status,
                                                         a.conc_erase, a.gated);
     return;

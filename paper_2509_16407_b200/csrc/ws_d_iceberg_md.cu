@@ -465,7 +465,7 @@ static void iceberg_md_ops(const OpsArgs& a, bool def) {
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.front + 255) / 256, 4);  // <= ~1 op in flight per front bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
     k_mixed_icemd_rounds<<<(unsigned)g, 256, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status, a.vout,
                                                         a.conc_erase, a.gated);
     return;
@@ -475,7 +475,7 @@ static void iceberg_md_ops(const OpsArgs& a, bool def) {
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.front + 255) / 256, 4);  // <= ~1 op in flight per front bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
     if (a.d.tune_l2pol == 2)
       k_erase_icemd_rounds<true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.status, a.conc_erase, a.gated);
     else
@@ -487,7 +487,7 @@ static void iceberg_md_ops(const OpsArgs& a, bool def) {
       a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
     k_upsert_icemd_rounds<true><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, a.n, a.uop >> 4, a.status,
                                                                a.conc_erase, a.gated);
     return;
@@ -499,7 +499,7 @@ static void iceberg_md_query(const QueryArgs& a, bool def) {
   // the generic one at 2^26, where the tag array is largely L2-resident
   if (def && a.d.tune_qilp == 6) {
     u64 g = (a.n + 255) / 256;
-    g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * kTableGridPerSM);
+    g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * table_grid_per_sm(a.d));
 #define WS_QI(RO, F) k_query_icemd_coop<RO, F><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, \
                                                                             a.conc_erase, a.gated)
     const bool f64 = a.d.tune_l2pol == 2;

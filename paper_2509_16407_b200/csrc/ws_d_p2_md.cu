@@ -20,7 +20,7 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
       !a.rlist && !a.d.phased && !a.d.lock_elided && a.d.tune_upsert == 4) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
     k_mixed_p2md_rounds<3><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status, a.vout,
                                                           a.conc_erase, a.gated);
     return;
@@ -29,7 +29,7 @@ static void p2_md_ops(const OpsArgs& a, bool def) {
       a.d.tune_upsert >= 2) {
     u64 g = (a.n + 255) / 256;
     const u64 lim = std::max<u64>((a.d.nb + 255) / 256, 4);  // <= ~1 op in flight per bucket
-    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * kTableGridPerSM), lim), 1);
+    g = std::max<u64>(std::min<u64>(std::min<u64>(g, (u64)kSMs * table_grid_per_sm(a.d)), lim), 1);
 #define WS_UR(F, PH, FI) k_upsert_p2md_rounds<F, 4, PH, FI><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.vals, \
                                                    a.n, a.uop >> 4, a.status, a.conc_erase, a.gated)
     if (a.d.phased) { if (a.d.tune_upsert >= 3) WS_UR(true, true, false); else WS_UR(false, true, false); }
@@ -48,7 +48,7 @@ static void p2_md_query(const QueryArgs& a, bool def) {
   }
   // one thread per op, pair-cooperative tag fetches
   u64 g = (a.n + 255) / 256;
-  g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * kTableGridPerSM);
+  g = std::min<u64>(std::max<u64>(g, 1), (u64)kSMs * table_grid_per_sm(a.d));
 #define WS_QC(RO, F) k_query_p2md_coop<RO, F, 5><<<(unsigned)g, 256, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, \
                                                                               a.conc_erase, a.gated, a.check_keys)
   const bool f64 = a.d.tune_l2pol == 2;

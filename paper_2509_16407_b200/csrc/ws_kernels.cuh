@@ -23,6 +23,16 @@ __host__ __device__ constexpr int default_bs(int design) {
 // 10.29 ms / 54.5 -> 43.6 ms and the insert 25.5 -> 24.2 ms / 101.2 -> 94.8
 // ms; the plateau starts near 96.
 constexpr int kTableGridPerSM = 256;
+// A launch whose batch size lives on the device (Dev::dn: the split's erase /
+// query segments, the multi-GPU exchange's per-source inbox segments) is
+// sized for its host-side UPPER bound, so much of a 256-per-SM grid would be
+// CTAs that read the count and exit; such launches keep 32 per SM and walk
+// their segment grid-stride (same-box A/B: aging and YCSB equal or better
+// than with the full grid, profiles/grid_size_r02.log).
+constexpr int kTableGridPerSMDev = 32;
+__host__ __device__ inline int table_grid_per_sm(const Dev& d) {
+  return d.dn ? kTableGridPerSMDev : kTableGridPerSM;
+}
 
 inline unsigned grid_for(u64 n, int threads = kThreads, int per_sm = 8) {
   u64 g = (n + threads - 1) / threads;
@@ -150,7 +160,7 @@ void launch_ops_t(const OpsArgs& a) {
                                                                   a.vout, a.redo, a.probes, a.lock_acc,
                                                                   a.conc_erase, a.gated);
   else
-    k_ops<DES, BS, false><<<a.serial ? 1 : grid_for_table(a.n, a.d.nb, kThreads, kTableGridPerSM), a.serial ? 1 : kThreads, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
+    k_ops<DES, BS, false><<<a.serial ? 1 : grid_for_table(a.n, a.d.nb, kThreads, table_grid_per_sm(a.d)), a.serial ? 1 : kThreads, 0, a.s>>>(a.d, a.ops, a.uop, a.keys, a.vals, a.n, a.status,
                                                                 a.vout, a.redo, a.probes, a.lock_acc,
                                                                 a.conc_erase, a.gated, a.rlist, a.rcount);
 }
@@ -158,10 +168,10 @@ void launch_ops_t(const OpsArgs& a) {
 template <int DES, int BS>
 void launch_query_t(const QueryArgs& a) {
   if (a.ro)
-    k_query<DES, BS, true><<<grid_for(a.n, kThreads, kTableGridPerSM), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase,
+    k_query<DES, BS, true><<<grid_for(a.n, kThreads, table_grid_per_sm(a.d)), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found, a.conc_erase,
                                                                  a.gated);
   else
-    k_query<DES, BS, false><<<grid_for(a.n, kThreads, kTableGridPerSM), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found,
+    k_query<DES, BS, false><<<grid_for(a.n, kThreads, table_grid_per_sm(a.d)), kThreads, 0, a.s>>>(a.d, a.keys, a.n, a.vout, a.found,
                                                                   a.conc_erase, a.gated);
 }
 
