@@ -349,6 +349,54 @@ def test_p2md_2pow28_fill_and_query_properties():
     assert t.duplicate_count() == 0
 
 
+def test_p2md_2pow28_tombstone_churn_properties():
+    """Config 2 size after churn: fill 2^28 slots to 0.9, erase every other
+    key (tombstones: the reference's shortcut and query early-out switch off,
+    openaddr.py:372-373, 440-442), upsert-ADD onto the survivors, then refill
+    the erased count with fresh keys that reuse tombstoned cells.  Checked
+    through size-independent properties: erase flags, statuses, the
+    occupied count and checksum equal numpy's over the expected contents,
+    every survivor carries value + delta, erased keys are gone, fresh keys
+    found, no duplicates."""
+    from paper_2509_16407_b200.core import TableConfig
+    from paper_2509_16407_b200.workload import mix64_np
+    cap = 1 << 28
+    t = _table(TableConfig(design="p2_md", capacity_slots=cap, seed=42))
+    n = int(cap * 0.9)
+    keys = _keys(777, n)
+    vals = keys & np.uint64(0xFFFF)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals)))
+    assert int((st == 2).sum()) <= 3 and not (st == 1).any() and not (st > 2).any()
+    keys, vals = keys[st == 0], vals[st == 0]
+    gone, kept = keys[0::2], keys[1::2]
+    kv = vals[1::2]
+    assert bool(t.erase_batch(_cuda(gone)).all())
+    delta = (kept >> np.uint64(40)) | np.uint64(1)
+    st = _np(t.upsert_batch(_cuda(kept), _cuda(delta), merge="add"))
+    assert (st == 1).all()
+    fresh = _keys(778, len(gone))
+    fv = fresh >> np.uint64(9)
+    st = _np(t.upsert_batch(_cuda(fresh), _cuda(fv)))
+    # every fresh key finds a tombstoned or empty cell: the table is back at 0.9
+    assert int((st == 2).sum()) <= 3 and not (st == 1).any() and not (st > 2).any()
+    ok = st == 0
+    with np.errstate(over="ignore"):
+        ki = np.concatenate([kept, fresh[ok]])
+        vi = np.concatenate([kv + delta, fv[ok]])
+        want = (len(ki), int(ki.sum(dtype=np.uint64)), int(vi.sum(dtype=np.uint64)),
+                int(np.bitwise_xor.reduce(mix64_np(ki ^ mix64_np(vi)))))
+    assert t.checksum() == want
+    found, got = t.query_batch(_cuda(kept))
+    assert bool(found.all())
+    np.testing.assert_array_equal(_np(got), kv + delta)
+    found, got = t.query_batch(_cuda(fresh))
+    np.testing.assert_array_equal(_np(found).astype(bool), ok)
+    np.testing.assert_array_equal(_np(got)[ok], fv[ok])
+    found, _ = t.query_batch(_cuda(gone))
+    assert int(found.sum()) == 0
+    assert t.duplicate_count() == 0
+
+
 def test_p2md_2pow30_north_star_size_properties():
     """The north-star size: 2^30 slots (18 GiB of table), 966,367,641 inserts
     to 0.9 in one batch, then every key queried plus 2^24 absent keys --
