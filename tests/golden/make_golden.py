@@ -113,14 +113,14 @@ def hash_kat():
         json.dump(out, fh, indent=0)
 
 
-def _cap_for(design, cap):
-    bs = rcore.DEFAULT_BUCKET_SIZE[design]
+def _cap_for(design, cap, bucket=0):
+    bs = bucket or rcore.DEFAULT_BUCKET_SIZE[design]
     return cap - cap % bs
 
 
-def run_stream(design, stream, cap, seed, n_ops, universe_frac, extra=None, fill=False):
-    cfg = rcore.TableConfig(design=design, capacity_slots=_cap_for(design, cap), seed=seed,
-                            **(extra or {}))
+def run_stream(design, stream, cap, seed, n_ops, universe_frac, extra=None, fill=False, out_name=None):
+    cfg = rcore.TableConfig(design=design, capacity_slots=_cap_for(design, cap, (extra or {}).get("bucket_size", 0)),
+                            seed=seed, **(extra or {}))
     t = make_table(cfg)
     rng = random.Random(seed * 1000 + len(stream))
     rec = ProbeRecorder(line_bytes=cfg.line_bytes)
@@ -182,7 +182,7 @@ def run_stream(design, stream, cap, seed, n_ops, universe_frac, extra=None, fill
             res["tags"] = np.array([t.tags.get(i) for i in range(t.capacity_slots)],
                                    dtype=np.uint16)
     res["extra"] = np.array([json.dumps(extra or {})])
-    np.savez_compressed(os.path.join(OUT, f"ops_{design}_{stream}.npz"), **res)
+    np.savez_compressed(os.path.join(OUT, out_name or f"ops_{design}_{stream}.npz"), **res)
     return res
 
 
