@@ -13,7 +13,8 @@ kernels serve (the tuned kernels are specialised to the default buckets).
    third key give the oracle's hit set, values and final map (the oracle
    minus any key the concurrent order legitimately reported FULL); on
    buckets of >= 8 slots an upsert batch with duplicate keys under a
-   commutative merge (add / max / min) in between.
+   commutative merge (add / max / min) in between; odd cases pass numpy host
+   batches (the staged host path of the C ABI), even cases device tensors.
 """
 
 import numpy as np
@@ -85,7 +86,10 @@ def test_device_concurrent_batches_fuzz_config(name, case, cfg):
         n = max(1, int(full[0]) // 2)
     keys = gen_uniform_keys(seed, n)
     vals = gen_uniform_keys(seed + 1, n)
-    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals)))
+    # odd cases pass host (numpy) batches: the C ABI's staged host path
+    host = int(name[:2]) % 2 == 1
+    dev = (lambda a: np.ascontiguousarray(a)) if host else _cuda
+    st = _np(t.upsert_batch(dev(keys), dev(vals)))
     ost = o.upsert_batch(keys, vals)
     assert (ost == 0).all()
     # distinct keys, so any linearisation is a valid outcome: the keys the
@@ -100,7 +104,7 @@ def test_device_concurrent_batches_fuzz_config(name, case, cfg):
         for k in keys[~ins]:
             o.erase(int(k))
     q = np.concatenate([keys[::2], gen_uniform_keys(seed + 2, n // 2 + 1)])
-    found, got = t.query_batch(_cuda(q))
+    found, got = t.query_batch(dev(q))
     of, ov = o.query_batch(q)
     np.testing.assert_array_equal(found.cpu().numpy().astype(bool), of.astype(bool))
     np.testing.assert_array_equal(_np(got), ov)
@@ -116,17 +120,17 @@ def test_device_concurrent_batches_fuzz_config(name, case, cfg):
         dup = np.concatenate([keys[::5], np.repeat(fresh, 3)])
         dup = dup[np.random.default_rng(seed).permutation(dup.size)]
         dv = gen_uniform_keys(seed + 4, dup.size)
-        st2 = _np(t.upsert_batch(_cuda(dup), _cuda(dv), merge=merge))
+        st2 = _np(t.upsert_batch(dev(dup), dev(dv), merge=merge))
         o.upsert_batch(dup, dv, merge=merge)
         assert set(np.unique(st2).tolist()) <= {0, 1, 2}, np.unique(st2)
         fk = np.unique(dup[st2 == 2])
         assert np.isin(fk, fresh).all() and fk.size <= max(1, fresh.size // 20), fk.size
         if fk.size:
-            t.erase_batch(_cuda(fk))
+            t.erase_batch(dev(fk))
             o.erase_batch(fk)
         assert int((st2 == 0).sum()) == fresh.size - fk.size
         assert dict(t.items()) == o.as_dict()
-    gone = t.erase_batch(_cuda(keys[::3]))
+    gone = t.erase_batch(dev(keys[::3]))
     ogone = o.erase_batch(keys[::3])
     np.testing.assert_array_equal(gone.cpu().numpy().astype(bool), ogone.astype(bool))
     assert dict(t.items()) == o.as_dict()
