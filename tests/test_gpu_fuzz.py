@@ -135,3 +135,77 @@ def test_device_concurrent_batches_fuzz_config(name, case, cfg):
     np.testing.assert_array_equal(gone.cpu().numpy().astype(bool), ogone.astype(bool))
     assert dict(t.items()) == o.as_dict()
     assert t.duplicate_scan() == {}
+
+
+# ----------------------------------------------------- tuned kernels, churn
+
+DEFAULT_DESIGNS = ["double", "double_md", "p2", "p2_md", "iceberg", "iceberg_md", "cuckoo", "chaining"]
+CHURN = [(d, s) for s in range(5) for d in DEFAULT_DESIGNS]
+
+
+def _apply_checked(t, o, kind, keys, vals=None, merge=None, dev=None):
+    """One concurrent batch of distinct keys on the device and the same batch
+    on the oracle.  FULL depends on the order at high load (any linearisation
+    of distinct-key ops is valid): a key FULL on one side only is taken out of
+    the other, and the caller bounds how often that happens."""
+    if kind == "upsert":
+        st = _np(t.upsert_batch(dev(keys), dev(vals), merge=merge))
+        ost = o.upsert_batch(keys, vals, merge=merge)
+        assert set(np.unique(st).tolist()) <= {0, 1, 2}
+        both = (st != 2) & (ost != 2)
+        np.testing.assert_array_equal(st[both], ost[both])
+        for k in keys[(st == 2) & (ost != 2)]:
+            o.erase(int(k))
+        only_o = keys[(st != 2) & (ost == 2)]
+        if only_o.size:
+            t.erase_batch(dev(only_o))
+        return int((~both).sum())
+    if kind == "erase":
+        got = t.erase_batch(dev(keys)).cpu().numpy().astype(bool)
+        np.testing.assert_array_equal(got, o.erase_batch(keys).astype(bool))
+        return 0
+    f, v = t.query_batch(dev(keys))
+    of, ov = o.query_batch(keys)
+    np.testing.assert_array_equal(f.cpu().numpy().astype(bool), of.astype(bool))
+    np.testing.assert_array_equal(_np(v), ov)
+    return 0
+
+
+@pytest.mark.parametrize("design,rep", CHURN, ids=[f"{d}-{s}" for d, s in CHURN])
+def test_tuned_kernels_random_size_churn(design, rep):
+    """Default knobs (the tuned lock-round / line-walk kernels), a random
+    power-of-two capacity 2^10..2^18 and fill 0.5..0.9, then tombstone churn:
+    erase a random 30%, refill with fresh keys plus ADD-upserts of live and
+    erased keys, and a 50/50 query batch after every step -- hit set, values,
+    statuses and the final map against the oracle."""
+    from oracle import OracleTable
+    from paper_2509_16407_b200 import make_table
+    from paper_2509_16407_b200.core import DEFAULT_BUCKET_SIZE, TableConfig
+    from paper_2509_16407_b200.workload import gen_uniform_keys
+    rng = np.random.default_rng(1000 * rep + DEFAULT_DESIGNS.index(design))
+    log2 = int(rng.integers(10, 19))
+    bs = DEFAULT_BUCKET_SIZE[design]
+    cap = (1 << log2) - ((1 << log2) % bs)
+    cfg = TableConfig(design=design, capacity_slots=cap, seed=int(rng.integers(1, 1 << 30)))
+    t, o = make_table(cfg), OracleTable(cfg)
+    host = rep % 3 == 2  # some cases through the staged host-buffer path
+    dev = (lambda a: np.ascontiguousarray(a)) if host else _cuda
+    load = float(rng.uniform(0.5, 0.9)) * (1.5 if design == "chaining" else 1.0)
+    n = int(cap * load)
+    s = int(rng.integers(1, 1 << 30))
+    keys = gen_uniform_keys(s, n)
+    fulls = _apply_checked(t, o, "upsert", keys, gen_uniform_keys(s + 1, n), dev=dev)
+    miss = gen_uniform_keys(s + 2, n // 2 + 1)
+    _apply_checked(t, o, "query", np.concatenate([keys[::2], miss]), dev=dev)
+    gone = keys[rng.random(n) < 0.3]
+    _apply_checked(t, o, "erase", gone, dev=dev)
+    fresh = gen_uniform_keys(s + 3, gone.size // 2 + 1)
+    live = np.setdiff1d(keys, gone)[: max(1, n // 10)]
+    again = gone[: gone.size // 3]
+    batch = np.unique(np.concatenate([fresh, live, again]))
+    batch = batch[rng.permutation(batch.size)]
+    fulls += _apply_checked(t, o, "upsert", batch, gen_uniform_keys(s + 4, batch.size), merge="add", dev=dev)
+    _apply_checked(t, o, "query", np.concatenate([keys, fresh, miss]), dev=dev)
+    assert fulls <= max(2, n // 500), fulls
+    assert dict(t.items()) == o.as_dict()
+    assert t.duplicate_scan() == {}
