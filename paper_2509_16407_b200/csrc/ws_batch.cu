@@ -498,11 +498,81 @@ __global__ void k_agg_expand(const u32* grp, const AggSlot* tab, const u32* __re
   }
 }
 
+// Large plain batches (round 2, "combining"): the
+// scratch table above is L2-resident only up to ~2M ops; past that every
+// aggregation atomic is a random DRAM access and combining a uniform batch
+// cost 3x the uncombined apply.  So a plain batch of more than kCombineChunk
+// ops is (1) validated once, then (2) for a commutative merge, whose result
+// does not depend on combining, sampled: kCombineSample keys at a fixed
+// stride go into a small hash set and if fewer than 1/64 of them repeat (no
+// hot keys: same-key ops rarely meet on a lock) the batch is applied
+// uncombined (same final map; the one INSERTED status of a new key may then
+// go to any of its ops, as in any concurrent batch); otherwise (3) combined
+// chunk by chunk, each chunk with an L2-resident scratch table.  Chunks apply
+// in batch order, so REPLACE / KEEP keep their serial last- / first-write
+// result and each key's first op in the batch is still the one reporting
+// INSERTED.
+constexpr u64 kCombineChunk = 1ull << 21;
+constexpr u32 kCombineSample = 1u << 16;
+constexpr u32 kSampleSetMask = (1u << 18) - 1;
+
+__global__ void k_sample_dups(const u64* __restrict__ keys, u64 stride, u64* set, u32* dups) {
+  const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kCombineSample) return;
+  const u64 key = __ldg(keys + (u64)i * stride);
+  u32 h = (u32)mix64(key) & kSampleSetMask;
+  for (;;) {  // 2^16 keys in 2^18 slots: short probes; key 0 (a sentinel) counts as placed
+    const u64 prev = atomicCAS((unsigned long long*)(set + h), 0ull, (unsigned long long)key);
+    if (prev == 0ull) return;
+    if (prev == key) { atomicAdd(dups, 1u); return; }
+    h = (h + 1) & kSampleSetMask;
+  }
+}
+
+int combine_chunk(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status, cudaStream_t s,
+                  u32 flags, const CallCtx& cx, const u32* oidx, const u64* dn, u64 nbatch);
+
 // one uniform upsert batch (merge = uop >> 4), combined; see above.  oidx /
 // dn / nbatch: a gathered segment (positions -> batch indices < nbatch, the
 // device-resident length dn); all null / 0 for a plain batch.
 int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status, cudaStream_t s,
                     u32 flags, const CallCtx& cx, const u32* oidx, const u64* dn, u64 nbatch) {
+  if (oidx || dn || n <= kCombineChunk)
+    return combine_chunk(t, uop, keys, vals, n, status, s, flags, cx, oidx, dn, nbatch);
+  int rc = validate(keys, nullptr, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
+  if (rc) return rc;
+  // the chunks run unchecked but stay gated on this call's verdict
+  const u32 sub = (flags & ~WS_F_SYNC_CHECK) | WS_F_NO_CHECK |
+                  ((flags & WS_F_NO_CHECK) && !(flags & kF_VALIDATED) ? 0u : kF_VALIDATED);
+  const int m = uop >> 4;
+  if (m == M_ADD || m == M_MAX || m == M_MIN) {
+    u64* set = nullptr;
+    if (cudaMallocAsync((void**)&set, 8ull * (kSampleSetMask + 1) + 64, s) != cudaSuccess) return WS_ERR_ALLOC;
+    u32* dups = (u32*)(set + kSampleSetMask + 1);
+    rc = cuda_err(cudaMemsetAsync(set, 0, 8ull * (kSampleSetMask + 1) + 64, s));
+    if (!rc) {
+      k_sample_dups<<<kCombineSample / 256, 256, 0, s>>>(keys, n / kCombineSample, set, dups);
+      rc = cuda_err(cudaGetLastError());
+    }
+    u64* hp = pin();
+    if (!rc && !hp) rc = WS_ERR_ALLOC;
+    if (!rc) rc = cuda_err(cudaMemcpyAsync(hp, dups, 4, cudaMemcpyDeviceToHost, s));
+    if (!rc) rc = cuda_err(cudaStreamSynchronize(s));
+    const u32 nd = rc ? 0u : *(const u32*)hp;
+    cudaFreeAsync(set, s);
+    if (rc) return rc;
+    if ((u64)nd * 64 < kCombineSample)
+      return run_device_plain(t, nullptr, uop, keys, vals, n, status, nullptr, s, sub & ~WS_F_COMBINE, false, true,
+                              false, cx);
+  }
+  for (u64 lo = 0; lo < n && !rc; lo += kCombineChunk)
+    rc = combine_chunk(t, uop, keys + lo, vals + lo, std::min(kCombineChunk, n - lo), status ? status + lo : nullptr,
+                       s, sub, cx, nullptr, nullptr, 0);
+  return rc;
+}
+
+int combine_chunk(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n, u8* status, cudaStream_t s,
+                  u32 flags, const CallCtx& cx, const u32* oidx, const u64* dn, u64 nbatch) {
   int rc = dn ? WS_OK : validate(keys, nullptr, n, s, (flags & WS_F_SYNC_CHECK) != 0, flags, cx);
   if (rc) return rc;
   // the folded batch keeps the kernels gated on this call's validation verdict

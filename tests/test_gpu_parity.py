@@ -504,6 +504,55 @@ def test_combined_hot_key_batch_matches_oracle(design, merge):
     assert t.duplicate_scan() == {}
 
 
+@pytest.mark.parametrize("merge", ["add", "max", "keep", None])
+@pytest.mark.parametrize("dist", ["zipf", "uniform"])
+def test_combined_large_batch_matches_serial_order(dist, merge):
+    """Batches past the combining chunk (2^21 ops): a commutative merge on a
+    batch without hot keys is applied uncombined (sampled), otherwise the
+    batch is combined chunk by chunk in batch order.  Either way: one
+    INSERTED per new key (on its first op for keep / replace), every other op
+    UPDATED, and the final map of the serial order (first / last write for
+    keep / replace)."""
+    from paper_2509_16407_b200.workload import zipf_ranks
+    n = (1 << 21) * 3 + 12345
+    cfg = cfg_for("p2_md", 1 << 23, seed=6)
+    t = _table(cfg)
+    if dist == "zipf":
+        uni = _keys(19, 1 << 20)
+        keys = uni[zipf_ranks(1 << 20, n, 0.99, seed=3) - 1]
+    else:  # every key about twice, spread over the batch
+        uni = _keys(21, n // 2)
+        keys = uni[np.random.default_rng(5).integers(0, uni.size, n)]
+    vals = (np.arange(n, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)
+    st = _np(t.upsert_batch(_cuda(keys), _cuda(vals), merge=merge, combine=True))
+    u, first, inv = np.unique(keys, return_index=True, return_inverse=True)
+    assert int((st == 2).sum()) == 0
+    # exactly one INSERTED per key; for keep / replace (always combined) it is
+    # the key's first op, for a commutative merge any one op of the key (the
+    # sampled batch may run uncombined, i.e. in a concurrent order)
+    assert (np.bincount(inv[st == 0], minlength=len(u)) == 1).all()
+    if merge in ("keep", None):
+        assert (st[first] == 0).all()
+    got_k, got_v = t.items_arrays()
+    order = np.argsort(got_k)
+    got_k, got_v = got_k[order], got_v[order]
+    np.testing.assert_array_equal(got_k, u)
+    if merge in ("add", "max"):
+        want = np.zeros(len(u), dtype=np.uint64)
+        idx = np.searchsorted(u, keys)
+        if merge == "add":
+            np.add.at(want, idx, vals)
+        else:
+            np.maximum.at(want, idx, vals)
+    elif merge == "keep":
+        want = vals[first]
+    else:  # replace: the last write
+        last = len(keys) - 1 - np.unique(keys[::-1], return_index=True)[1]
+        want = vals[last]
+    np.testing.assert_array_equal(got_v, want)
+    assert t.duplicate_scan() == {}
+
+
 def test_tombstoned_small_table_upserts_make_progress():
     """After erases the shortcut is off, so every P2-MD insert locks its
     alternate bucket too; in a small table lanes of one warp cross-lock each
