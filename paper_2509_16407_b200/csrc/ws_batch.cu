@@ -502,12 +502,13 @@ __global__ void k_agg_expand(const u32* grp, const AggSlot* tab, const u32* __re
 // scratch table above is L2-resident only up to ~2M ops; past that every
 // aggregation atomic is a random DRAM access and combining a uniform batch
 // cost 3x the uncombined apply.  So a plain batch of more than kCombineChunk
-// ops is (1) validated once, then (2) for a commutative merge, whose result
-// does not depend on combining, sampled: kCombineSample keys at a fixed
-// stride go into a small hash set and if fewer than 1/64 of them repeat (no
-// hot keys: same-key ops rarely meet on a lock) the batch is applied
-// uncombined (same final map; the one INSERTED status of a new key may then
-// go to any of its ops, as in any concurrent batch); otherwise (3) combined
+// ops is (1) validated once, (2) sampled: kCombineSample keys at a fixed
+// stride go into a small hash set.  If fewer than 1/64 of them repeat (no hot
+// keys: same-key ops rarely meet on a lock) and the merge is commutative, so
+// the result does not depend on combining, the batch is applied uncombined
+// (same final map; the one INSERTED status of a new key may then go to any
+// of its ops, as in any concurrent batch).  If at least 1/4 repeat (heavy
+// skew, few distinct keys) it is folded whole.  Otherwise (3) it is combined
 // chunk by chunk, each chunk with an L2-resident scratch table.  Chunks apply
 // in batch order, so REPLACE / KEEP keep their serial last- / first-write
 // result and each key's first op in the batch is still the one reporting
@@ -545,7 +546,8 @@ int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n
   const u32 sub = (flags & ~WS_F_SYNC_CHECK) | WS_F_NO_CHECK |
                   ((flags & WS_F_NO_CHECK) && !(flags & kF_VALIDATED) ? 0u : kF_VALIDATED);
   const int m = uop >> 4;
-  if (m == M_ADD || m == M_MAX || m == M_MIN) {
+  const bool commutative = m == M_ADD || m == M_MAX || m == M_MIN;
+  {
     u64* set = nullptr;
     if (cudaMallocAsync((void**)&set, 8ull * (kSampleSetMask + 1) + 64, s) != cudaSuccess) return WS_ERR_ALLOC;
     u32* dups = (u32*)(set + kSampleSetMask + 1);
@@ -561,9 +563,13 @@ int combine_uniform(ws_table* t, u8 uop, const u64* keys, const u64* vals, u64 n
     const u32 nd = rc ? 0u : *(const u32*)hp;
     cudaFreeAsync(set, s);
     if (rc) return rc;
-    if ((u64)nd * 64 < kCombineSample)
+    if (commutative && (u64)nd * 64 < kCombineSample)
       return run_device_plain(t, nullptr, uop, keys, vals, n, status, nullptr, s, sub & ~WS_F_COMBINE, false, true,
                               false, cx);
+    // heavily skewed (>= 1/4 of the sample repeats): few distinct keys, so
+    // one whole-batch fold touches few scratch slots and applies each hot key
+    // once, where chunks would re-apply it per chunk
+    if ((u64)nd * 4 >= kCombineSample) return combine_chunk(t, uop, keys, vals, n, status, s, sub, cx, nullptr, nullptr, 0);
   }
   for (u64 lo = 0; lo < n && !rc; lo += kCombineChunk)
     rc = combine_chunk(t, uop, keys + lo, vals + lo, std::min(kCombineChunk, n - lo), status ? status + lo : nullptr,
